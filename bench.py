@@ -1,0 +1,306 @@
+#!/usr/bin/env python
+"""Benchmark of the fused Fourier bilateral filter (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl ours|reference]
+
+A "step" is one pass of the filtering hot path over one image of the
+configuration (default c1: 2048x2048 Voronoi image, theta=5, sigma=50, fixed
+K=4, T=203 from the host optimiser). Multi-GPU (torchrun, one process per GPU):
+every rank filters its own independent image of that configuration (frames
+shard one-per-GPU, no collective) -> weak scaling; value = all ranks' pixels /
+max-over-ranks time.
+
+Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA events on
+the launching stream, with a 256 MiB L2 flush (memset) between steps outside
+the events; barrier + synchronize on both sides; max over ranks.
+  value      : device-resident megapixels/s (input already in HBM)
+  e2e        : the same metric through the public host-buffer API
+               (fbf_fast_bilateral_f32: pinned H2D + validate + kernel + D2H)
+  roofline   : algorithmic FP32 FLOPs of the fused kernel ((4K-2)*2*(2r+1)*2
+               per pixel) / mean launch time, vs the FP32-FMA peak
+  cpu_baseline: the reference's own fast_bilateral (oracle/_ref, compiled
+               verbatim, all host threads) on the same image, rank 0, N=1.
+--impl reference times that CPU reference as the run itself.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAK_SM_MHZ_FALLBACK = 1965.0
+FP32_LANES_PER_SM = 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.01):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.period = period_s
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_reference_run(img, cfg, approx, seconds: float, min_reps: int = 1):
+    """Time the reference's fast_bilateral (or the C port) on the host cores."""
+    import numpy as np
+    from oracle import fbf_oracle
+    threads = os.cpu_count() or 1
+    img64 = np.ascontiguousarray(img, dtype=np.float64)
+    if fbf_oracle.RefLibrary.available():
+        lib, kind = fbf_oracle.RefLibrary(), "reference"
+        run = lambda: lib.fast_bilateral(img64, cfg.theta, approx.terms, approx.half_period, approx.coefficients,
+                                         threads=threads)
+    else:
+        lib, kind, threads = fbf_oracle.Oracle(), "port", 1
+        run = lambda: lib.fast_bilateral(img64, cfg.theta, approx.terms, approx.half_period, approx.coefficients)
+    times = []
+    t_end = time.perf_counter() + seconds
+    while len(times) < min_reps or time.perf_counter() < t_end:
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    return kind, threads, times
+
+
+def run_reference_impl(args, cfg):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    from paper_1811_02168_b200 import configs
+    img = configs.make_frame(cfg, 0)
+    approx = configs.select(cfg)
+    _, _, wt = cpu_reference_run(img, cfg, approx, 0.0, min_reps=max(0, args.warmup))
+    kind, threads, times = cpu_reference_run(img, cfg, approx, 0.0, min_reps=args.steps)
+    total = sum(times)
+    mp = cfg.width * cfg.height * len(times) / total / 1e6
+    line = {
+        "metric": "megapixels_per_sec", "value": round(mp, 4), "unit": "MP/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.width}x{cfg.height} {cfg.generator} image, theta={cfg.theta}, "
+                               f"sigma={cfg.sigma}, K={approx.terms}, T={approx.half_period}, symmetric border"},
+        "cpu_baseline": {"value": round(mp, 4), "unit": "MP/s", "cores": threads, "kind": kind,
+                         "sample": f"one full {cfg.width}x{cfg.height} image per step"},
+        "e2e": {"value": round(mp, 4), "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    from paper_1811_02168_b200 import configs
+    cfg = configs.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_impl(args, cfg)
+        return
+
+    rank, world, local = dist_env()
+    import numpy as np
+    import torch
+    import paper_1811_02168_b200 as fb
+    from paper_1811_02168_b200 import _lib
+
+    lib = _lib.load()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    fb_check = lib.fbf_set_device(local)
+    if fb_check != 0:
+        raise RuntimeError(_lib.last_error())
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # per-rank independent image (frame `rank` of the config's generator)
+    img = configs.make_frame(cfg, rank)
+    approx = configs.select(cfg)
+    kernel = fb.build_spatial_kernel(cfg.theta)
+    H, W = img.shape
+    pixels = H * W
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(dev)
+    d_in = torch.from_numpy(img).to(dev)
+    d_out = torch.empty_like(d_in)
+    d_fb = torch.zeros(1, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    fb.validate_device(d_in)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            flush.zero_()
+            fb.fast_bilateral_device(d_in, kernel, approx, d_out, d_fallbacks=d_fb, stream=stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = lib.fbf_kernel_launches()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        with torch.cuda.stream(stream):
+            for s in range(args.steps):
+                flush.zero_()
+                ev[s][0].record(stream)
+                fb.fast_bilateral_device(d_in, kernel, approx, d_out, d_fallbacks=d_fb, stream=stream)
+                ev[s][1].record(stream)
+        torch.cuda.synchronize(dev)
+    launches = lib.fbf_kernel_launches() - launches0
+    barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms_max = float(t.item())
+    value = world * pixels * args.steps / (total_ms_max * 1e-3) / 1e6
+
+    # ---- e2e through the host-buffer public API (pinned H2D + D2H inside) ----
+    h_in = torch.from_numpy(img).pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    a_in, a_out = h_in.numpy(), h_out.numpy()
+    for _ in range(2):
+        fb.fast_bilateral(a_in, kernel, approx, out=a_out)
+    barrier()
+    e2e_times = []
+    diag = fb.FilterDiagnostics()
+    for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        fb.fast_bilateral(a_in, kernel, approx, diag=diag, out=a_out)
+        e2e_times.append(time.perf_counter() - t0)
+    barrier()
+    e2e_total = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(e2e_total, op=dist.ReduceOp.MAX)
+    e2e_value = world * pixels * args.e2e_steps / float(e2e_total.item()) / 1e6
+
+    if rank == 0:
+        flop_px = cfg.flop_per_pixel(approx.terms)
+        mean_launch_s = (total_ms / args.steps) * 1e-3 / max(1, launches // max(1, args.steps))
+        per_launch_flop = flop_px * pixels / max(1, launches // max(1, args.steps))
+        achieved = per_launch_flop / mean_launch_s / 1e12
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        peaks = measured_peaks()
+        sm_max = peaks.get("sm_max_mhz", PEAK_SM_MHZ_FALLBACK)
+        peak = n_sm * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(prof):
+            with open(prof) as f:
+                traffic = json.load(f).get(cfg.name)
+        line = {
+            "metric": "megapixels_per_sec", "value": round(value, 2), "unit": "MP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms_max / args.steps, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": f"synthetic ({cfg.generator}, {cfg.sites} sites, noise {cfg.noise}, seed {cfg.frame_seed(rank)}+rank)",
+            "config": {"workload": f"{cfg.name}: {W}x{H} image per GPU, theta={cfg.theta} (r={cfg.radius}), "
+                                   f"sigma={cfg.sigma}, K={approx.terms}, T={approx.half_period}, "
+                                   f"{4 * approx.terms - 2} channels, symmetric border",
+                       "l2": "256 MiB memset flush between timed steps (outside the events)",
+                       "parallelism": f"frames one-per-GPU x{world}, no collective"},
+            "gpu_launches": int(launches),
+            "e2e": {"value": round(e2e_value, 2), "unit": "MP/s", "h2d_bytes_per_step": pixels * 4,
+                    "d2h_bytes_per_step": pixels * 4 + 16},
+            "roofline": {"bound": "fp32-fma", "achieved": round(achieved, 3), "peak": round(peak, 2),
+                         "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "flop_per_pixel": flop_px,
+                         "peak_source": f"{n_sm} SMs x 128 FP32 lanes x 2 x sm_max {sm_max} MHz "
+                                        "(MEASURED_PEAKS.json clock; FFMA2 microbench: profiles/r01_fma_peak.jsonl)"},
+            "clocks": clocks.summary(),
+            "fallback_pixels": int(diag.fallback_pixels),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            kind, threads, times = cpu_reference_run(img, cfg, approx, args.cpu_seconds)
+            mp = pixels * len(times) / sum(times) / 1e6
+            line["cpu_baseline"] = {"value": round(mp, 4), "unit": "MP/s", "cores": threads, "kind": kind,
+                                    "sample": f"{len(times)} x full {W}x{H} image, fp64 fast_bilateral"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,170 @@
+/*
+ * fbf.h -- C ABI of the B200-native Fourier bilateral filtering stage
+ * (arXiv 1811.02168), a drop-in for the reference fourierbf library's
+ * filtering path (/root/reference/proj). Plain pointers and sizes only; no C++
+ * or torch types cross this boundary, and no exception escapes it.
+ *
+ * Every entry point names the reference interface it replaces (file:line,
+ * paths relative to /root/reference/proj). Status codes replace the
+ * reference's exceptions; fbf_last_error() returns the message of the last
+ * failure on the calling thread.
+ *
+ * Buffers: images are row-major, at(x, y) = pixels[y * width + x]
+ * (include/fourierbf/image.hpp:25-26), single channel, float32 (the reference
+ * uses double; the oracle widens float -> double exactly). Host buffers are
+ * caller-owned; device buffers and streams are owned by a per-device context
+ * inside the library.
+ */
+#ifndef FBF_H
+#define FBF_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (exceptions in the reference) ------------------------- */
+#define FBF_OK 0
+#define FBF_EINVAL 1       /* std::invalid_argument (filter.cpp:132-134, kernels.cpp:13-14,106-107) */
+#define FBF_ERANGE 2       /* pixel non-finite or outside [0, R] (filter.cpp:19-23) */
+#define FBF_EUNREACHABLE 3 /* ToleranceUnreachable (approx.hpp:97-103); outputs hold the best fit */
+#define FBF_ECUDA 4        /* CUDA runtime failure or no device */
+#define FBF_ENOMEM 5
+#define FBF_ECAPACITY 6    /* caller buffer too small / radius beyond the kernel's limit */
+
+/* BorderPolicy (image.hpp:38), same order. */
+#define FBF_BORDER_SYMMETRIC 0
+#define FBF_BORDER_REPLICATE 1
+#define FBF_BORDER_ZERO 2
+
+/* RangeKernelKind (kernels.hpp:8), parametric kinds. */
+#define FBF_KERNEL_GAUSSIAN 0
+#define FBF_KERNEL_EXPONENTIAL 1
+#define FBF_KERNEL_CAUCHY 2
+
+/* Largest spatial radius ceil(3 theta) the fused sm_100a kernel is built for. */
+#define FBF_MAX_RADIUS 32
+
+/* Message of the last failed call on this thread ("" if none). */
+const char* fbf_last_error(void);
+/* Library / device info: number of visible CUDA devices (0 if none). */
+int fbf_device_count(void);
+/* Device used by the single-device host-buffer entry points
+ * (fbf_fast_bilateral_f32, fbf_filter); default 0. One process per GPU sets
+ * its local rank here. */
+int fbf_set_device(int device);
+int fbf_get_device(void);
+/* Number of fused-kernel launches this process has issued (all devices). */
+unsigned long long fbf_kernel_launches(void);
+
+/* ---- L1 kernels: kernels.cpp ------------------------------------------- */
+/* build_spatial_kernel (kernels.cpp:105-118): radius = ceil(3 theta); writes
+ * 2*radius+1 unnormalised taps. Returns the radius, or -FBF_EINVAL /
+ * -FBF_ECAPACITY (cap too small). */
+int fbf_build_spatial_kernel(double theta, double* taps, int cap);
+/* sample_range_kernel (kernels.cpp:78-103) for the parametric kinds:
+ * values[2R+1] = phi(t - R), exactly symmetric. */
+int fbf_sample_range_kernel(int kind, double sigma, int R, double* values);
+
+/* ---- L2 approximation: approx.cpp (host, restated without Eigen) --------- */
+/* nu = 2 pi / (2T+1) (approx.cpp:17-19). */
+double fbf_frequency_of(int half_period);
+/* fit_fixed_period (approx.cpp:105-117): least-squares c[K] at fixed (K, T);
+ * err_out = ||A c - b||^2. samples has 2R+1 entries. */
+int fbf_fit_fixed_period(const double* samples, int R, int K, int T, double* coeffs, double* err_out);
+/* scan_period_errors (approx.cpp:119-130): errors[T-1] = E(K, T), T = 1..t_max. */
+int fbf_scan_period_errors(const double* samples, int R, int K, int t_max, int threads, double* errors);
+/* min_error_over_period (approx.cpp:132-144): ties keep the smaller T. */
+int fbf_min_error_over_period(const double* samples, int R, int K, int t_max, int threads,
+                              int* T_best, double* err_out);
+/* optimize_parameters (approx.cpp:179-240), Algorithm 1. t_max<=0 -> 10R,
+ * k_max<=0 -> 2R+1. Returns FBF_EUNREACHABLE with the best fit when no
+ * K <= min(k_max, t_max+1) reaches tol. per_order (optional, 3*cap doubles)
+ * receives (K, T_best, e(K)) rows; *n_orders their count. */
+int fbf_optimize_parameters(const double* samples, int R, double tol, int t_max, int k_max,
+                            int threads, int* K_out, int* T_out, double* coeffs, int coeff_cap,
+                            double* err_out, double* per_order, int* n_orders);
+/* CLI select_parameters (tools/fourierbf.cpp:185-234):
+ *   eps>0, K=T=0      -> Algorithm 1 at tolerance eps
+ *   K>0, T=0          -> best T over 1..10R, then fit
+ *   K>0, T>0          -> fixed period
+ *   method_fbf != 0   -> T = R with K given (or K* from eps)
+ * eps together with K/T, or T without K, is FBF_EINVAL (as in the CLI). */
+int fbf_select_params(int kind, double sigma, int R, double eps, int K, int T, int method_fbf,
+                      int threads, int* K_out, int* T_out, double* coeffs, int coeff_cap,
+                      double* err_out);
+
+/* ---- L3 filter: filter.cpp (the hot path, sm_100a) ---------------------- */
+/* fast_bilateral (filter.hpp:43-46, filter.cpp:129-213) on HOST buffers:
+ * validates intensities, copies img to the device, runs the fused kernel,
+ * copies out back. K >= 1 coefficients c_0..c_{K-1}, T >= 1, R >= 1.
+ * *fallbacks (optional) is INCREMENTED by the number of pixels whose
+ * denominator was <= 1e-12 (FilterDiagnostics, filter.hpp:15-17). */
+int fbf_fast_bilateral_f32(const float* img, int width, int height, double theta, int K, int T,
+                           int R, const double* coeffs, int border, float* out,
+                           long long* fallbacks);
+/* Same, device-resident: d_img / d_out are device pointers on device `device`;
+ * enqueued on `stream` (a cudaStream_t; NULL = the legacy default stream)
+ * and returns without synchronising.
+ * d_fallbacks (optional) is a device unsigned long long counter that is
+ * atomically incremented. No intensity validation (use fbf_validate_f32). */
+int fbf_fast_bilateral_f32_device(const float* d_img, int width, int height, double theta, int K,
+                                  int T, int R, const double* coeffs, int border, float* d_out,
+                                  unsigned long long* d_fallbacks, int device, void* stream);
+/* Batch of n_frames independent frames (frame f at img + f*width*height),
+ * sharded across the first n_gpus devices (0 -> all), one host thread each.
+ * Output frames land in disjoint slices of out. */
+int fbf_fast_bilateral_batch_f32(const float* img, int n_frames, int width, int height,
+                                 double theta, int K, int T, int R, const double* coeffs,
+                                 int border, float* out, long long* fallbacks, int n_gpus);
+/* One large image split into n_gpus row bands, each staged with replicated
+ * ceil(3 theta)-row halos (border rows keep the mirror semantics); no
+ * collective, outputs are disjoint row slices. Bit-identical to n_gpus = 1. */
+int fbf_fast_bilateral_bands_f32(const float* img, int width, int height, double theta, int K,
+                                 int T, int R, const double* coeffs, int border, float* out,
+                                 long long* fallbacks, int n_gpus);
+/* Device-resident band for one rank: d_src holds global rows
+ * [src_row0, src_row0 + src_rows) of a width x height image (row pitch =
+ * width) and must contain every row the border mapping reaches for output rows
+ * [out_row0, out_row0 + out_rows); d_dst receives those output rows. Use
+ * fbf_band_source_rows() to size the halo. */
+int fbf_fast_bilateral_band_f32_device(const float* d_src, int src_row0, int src_rows,
+                                       int width, int height, int out_row0, int out_rows,
+                                       double theta, int K, int T, int R, const double* coeffs,
+                                       int border, float* d_dst,
+                                       unsigned long long* d_fallbacks, int device, void* stream);
+/* Global source-row window [*row0, *row0 + *rows) needed for output rows
+ * [out_row0, out_row0 + out_rows) at radius ceil(3 theta). */
+int fbf_band_source_rows(int height, int out_row0, int out_rows, double theta, int border,
+                         int* row0, int* rows);
+/* Convenience signature from the north star: parameters chosen on the host
+ * like the CLI's `filter --eps` (eps_or_K < 1: tolerance) or `--K` (integer
+ * eps_or_K >= 1: fixed K, T scanned over 1..10R); Gaussian range kernel,
+ * R = 255, symmetric border. */
+int fbf_filter(const float* img, int height, int width, double theta, double sigma,
+               double eps_or_K, float* out);
+
+/* validate_intensities (filter.cpp:19-23) on the device: returns FBF_OK or
+ * FBF_ERANGE. */
+int fbf_validate_f32_device(const float* d_img, size_t n, int R, int device, void* stream);
+
+/* ---- L4 synthetic inputs (synthetic.cpp + BASELINE.json generators) ------ */
+/* random_image (synthetic.cpp:25-31), scene_image (:33-64), as float32. */
+void fbf_random_image_f32(int width, int height, unsigned long long seed, float* out);
+void fbf_scene_image_f32(int width, int height, unsigned long long seed, float* out);
+/* BASELINE configs 0/1/3: n_sites Voronoi cells with U(0,255) values,
+ * + N(0, noise^2), clipped to [0,255]. */
+void fbf_voronoi_image_f32(int width, int height, int n_sites, double noise, unsigned long long seed,
+                           int threads, float* out);
+/* BASELINE configs 2/4: sum of 32 seeded 2-D sinusoids scaled to [0,255],
+ * + n_sites Voronoi step edges (per-cell offset U(-64,64)), + N(0, noise^2),
+ * clipped to [0,255]. */
+void fbf_field_image_f32(int width, int height, int n_sites, double noise, unsigned long long seed,
+                         int threads, float* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FBF_H */

@@ -1,0 +1,103 @@
+"""Builds libfbf.so (the fbf C ABI: host C++ + sm_100a CUDA) in-tree.
+
+    python -m paper_1811_02168_b200.build [--force] [--jobs N]
+
+nvcc cross-compiles for sm_100a without a GPU. The 32 radius
+specialisations of the fused kernel are split across several translation units
+so they compile in parallel. The shared library is written next to this file
+(git-ignored; it travels to the GPU box with the repo snapshot).
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+BUILD = os.path.join(ROOT, "build", "fbf")
+LIB = os.path.join(HERE, "libfbf.so")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
+                     f"-I{os.path.join(ROOT, 'include')}"]
+CXX_FLAGS = ["-O3", "-std=c++20", "-fPIC", "-pthread", f"-I{os.path.join(ROOT, 'include')}"]
+# radius ranges per kernel translation unit (big radii are the slow ones)
+RADIUS_SPLITS = [(1, 8), (9, 12), (13, 15), (16, 18), (19, 21), (22, 24), (25, 26), (27, 28),
+                 (29, 30), (31, 32)]
+
+
+def _nvcc() -> str:
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if c and os.path.exists(c):
+            return c
+    raise RuntimeError("nvcc not found")
+
+
+def _deps() -> list[str]:
+    return [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "fbf.h")]
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd: list[str], log: str) -> None:
+    p = subprocess.run(cmd, capture_output=True, text=True)
+    with open(log, "w") as f:
+        f.write(" ".join(cmd) + "\n" + p.stdout + p.stderr)
+    if p.returncode != 0:
+        raise RuntimeError(f"build failed: {' '.join(cmd)}\n{p.stdout}{p.stderr}")
+
+
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
+    deps = _deps()
+    if not force and not _stale(LIB, deps):
+        return LIB
+    os.makedirs(BUILD, exist_ok=True)
+    nvcc = _nvcc()
+    jobs = jobs or min(len(RADIUS_SPLITS) + 3, os.cpu_count() or 4)
+    tasks = []
+    objs = []
+    for lo, hi in RADIUS_SPLITS:
+        obj = os.path.join(BUILD, f"fbf_kernel_r{lo:02d}_{hi:02d}.o")
+        objs.append(obj)
+        tasks.append(([nvcc, *NVCC_FLAGS, f"-DFBF_R_LO={lo}", f"-DFBF_R_HI={hi}", "-c",
+                       os.path.join(CSRC, "fbf_kernel_inst.cu"), "-o", obj], obj + ".log"))
+    obj = os.path.join(BUILD, "fbf_api.o")
+    objs.append(obj)
+    tasks.append(([nvcc, *NVCC_FLAGS, "-c", os.path.join(CSRC, "fbf_api.cu"), "-o", obj], obj + ".log"))
+    for src in ("fbf_params.cpp", "fbf_synth.cpp"):
+        obj = os.path.join(BUILD, src.replace(".cpp", ".o"))
+        objs.append(obj)
+        tasks.append((["g++", *CXX_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj], obj + ".log"))
+    with cf.ThreadPoolExecutor(jobs) as ex:
+        futs = [ex.submit(_run, cmd, log) for cmd, log in tasks]
+        for f in futs:
+            f.result()
+    tmp = LIB + ".tmp"
+    _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lpthread"],
+         os.path.join(BUILD, "link.log"))
+    os.replace(tmp, LIB)
+    if verbose:
+        print(f"built {LIB}")
+    return LIB
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--jobs", type=int, default=None)
+    a = ap.parse_args()
+    print(build(force=a.force, jobs=a.jobs, verbose=True))
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,569 @@
+// fbf_api.cu -- host side of the filtering path behind the C ABI (include/fbf.h).
+//
+// Mirrors fbf::fast_bilateral (/root/reference/proj/include/fourierbf/filter.hpp:43-46,
+// src/filter.cpp:129-213): argument checks and error classes follow the
+// reference (invalid_argument -> FBF_EINVAL, pixel range -> FBF_ERANGE), the
+// numerical work runs in the fused sm_100a kernel (fbf_kernel.cuh).
+//
+// One context per CUDA device owns a stream, a cached device arena and a
+// pinned counter block; calls on the same device serialise on its mutex, calls
+// on different devices run concurrently. Multi-GPU entry points start one host
+// thread per device: frames round-robin in contiguous blocks, or row bands with
+// replicated radius-row halos. There is no collective: outputs are disjoint.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <atomic>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/fbf.h"
+#include "fbf_internal.h"
+#include "fbf_kernel.cuh"
+
+namespace fbf_dev {
+#define FBF_EXTERN(R) extern template cudaError_t launch_fused<R>(const Params&, int, cudaStream_t);
+FBF_EXTERN(1) FBF_EXTERN(2) FBF_EXTERN(3) FBF_EXTERN(4) FBF_EXTERN(5) FBF_EXTERN(6) FBF_EXTERN(7)
+FBF_EXTERN(8) FBF_EXTERN(9) FBF_EXTERN(10) FBF_EXTERN(11) FBF_EXTERN(12) FBF_EXTERN(13)
+FBF_EXTERN(14) FBF_EXTERN(15) FBF_EXTERN(16) FBF_EXTERN(17) FBF_EXTERN(18) FBF_EXTERN(19)
+FBF_EXTERN(20) FBF_EXTERN(21) FBF_EXTERN(22) FBF_EXTERN(23) FBF_EXTERN(24) FBF_EXTERN(25)
+FBF_EXTERN(26) FBF_EXTERN(27) FBF_EXTERN(28) FBF_EXTERN(29) FBF_EXTERN(30) FBF_EXTERN(31)
+FBF_EXTERN(32)
+#undef FBF_EXTERN
+
+namespace {
+
+using LaunchFn = cudaError_t (*)(const Params&, int, cudaStream_t);
+struct RadiusEntry {
+    LaunchFn launch;
+    int max_pairs;
+    size_t pair_bytes, fixed_bytes;
+};
+
+template <int R>
+RadiusEntry entry() {
+    return {&launch_fused<R>, Geometry<R>::max_pairs(), Geometry<R>::pair_bytes, Geometry<R>::fixed_bytes};
+}
+
+const RadiusEntry& radius_entry(int r) {
+    static const RadiusEntry table[kMaxRadius + 1] = {
+        {nullptr, 0, 0, 0}, entry<1>(),  entry<2>(),  entry<3>(),  entry<4>(),  entry<5>(),
+        entry<6>(),  entry<7>(),  entry<8>(),  entry<9>(),  entry<10>(), entry<11>(),
+        entry<12>(), entry<13>(), entry<14>(), entry<15>(), entry<16>(), entry<17>(),
+        entry<18>(), entry<19>(), entry<20>(), entry<21>(), entry<22>(), entry<23>(),
+        entry<24>(), entry<25>(), entry<26>(), entry<27>(), entry<28>(), entry<29>(),
+        entry<30>(), entry<31>(), entry<32>()};
+    return table[r];
+}
+
+// filter.cpp:19-23 on the device: flag any non-finite pixel or one outside [0, R]
+__global__ void validate_kernel(const float* __restrict__ img, size_t n, float R, unsigned int* flag) {
+    bool bad = false;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const float v = img[i];
+        bad |= !(isfinite(v) && v >= 0.f && v <= R);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
+}  // namespace
+}  // namespace fbf_dev
+
+namespace fbf_b200 {
+namespace {
+
+using fbf_dev::kTW;
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(FBF_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define FBF_CUDA(call, what)                                    \
+    do {                                                        \
+        cudaError_t e_ = (call);                                \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what);      \
+    } while (0)
+
+struct DeviceCtx {
+    int device = 0;
+    int num_sms = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex mtx;
+    void* arena = nullptr;  // cached device scratch
+    size_t arena_bytes = 0;
+    unsigned long long* d_counters = nullptr;  // [0] fallbacks, [1] range flag
+    unsigned long long* h_counters = nullptr;  // pinned mirror
+
+    int init(int dev) {
+        device = dev;
+        FBF_CUDA(cudaSetDevice(dev), "cudaSetDevice");
+        FBF_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+        FBF_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        FBF_CUDA(cudaMalloc(&d_counters, 2 * sizeof(unsigned long long)), "cudaMalloc counters");
+        FBF_CUDA(cudaMallocHost(&h_counters, 2 * sizeof(unsigned long long)), "cudaMallocHost");
+        return FBF_OK;
+    }
+    int reserve(size_t bytes) {
+        if (bytes <= arena_bytes) return FBF_OK;
+        if (arena) cudaFree(arena);
+        arena = nullptr;
+        arena_bytes = 0;
+        const size_t want = bytes + bytes / 8;
+        if (cudaMalloc(&arena, want) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(FBF_ENOMEM, "device arena allocation of " + std::to_string(want) + " bytes failed");
+        }
+        arena_bytes = want;
+        return FBF_OK;
+    }
+};
+
+std::mutex g_ctx_mtx;
+std::vector<std::unique_ptr<DeviceCtx>> g_ctx;
+std::atomic<int> g_default_device{0};
+std::atomic<unsigned long long> g_launches{0};
+
+int get_ctx(int dev, DeviceCtx** out) {
+    std::lock_guard<std::mutex> lock(g_ctx_mtx);
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(FBF_ECUDA, "no CUDA device available (the fbf filter has no CPU fallback)");
+    }
+    if (dev < 0 || dev >= n) return fail(FBF_EINVAL, "device index out of range");
+    if ((int)g_ctx.size() < n) g_ctx.resize(n);
+    if (!g_ctx[dev]) {
+        auto c = std::make_unique<DeviceCtx>();
+        const int rc = c->init(dev);
+        if (rc != FBF_OK) return rc;
+        g_ctx[dev] = std::move(c);
+    }
+    *out = g_ctx[dev].get();
+    return FBF_OK;
+}
+
+// ---- launch planning -------------------------------------------------------
+
+struct Approx {
+    int K = 0, T = 0, R = 0;
+    std::vector<double> c;
+};
+
+int check_args(int width, int height, double theta, int K, int T, int R, const double* coeffs,
+               int border, int* radius) {
+    // filter.cpp:132-134, kernels.cpp:106-107, image.hpp:21-22
+    if (width <= 0 || height <= 0) return fail(FBF_EINVAL, "GrayImage: dimensions must be positive");
+    if (!(theta > 0.0) || !std::isfinite(theta)) return fail(FBF_EINVAL, "spatial kernel: theta must be positive");
+    if (K < 1 || T < 1 || R < 1 || !coeffs) return fail(FBF_EINVAL, "fast_bilateral: malformed approximation");
+    if (border < 0 || border > 2) return fail(FBF_EINVAL, "unknown border policy");
+    const int r = (int)std::ceil(3.0 * theta);
+    if (r > fbf_dev::kMaxRadius)
+        return fail(FBF_ECAPACITY, "spatial radius " + std::to_string(r) + " exceeds the kernel limit " +
+                                       std::to_string(fbf_dev::kMaxRadius));
+    *radius = r;
+    return FBF_OK;
+}
+
+struct Chunk {
+    int k_lo, n_k, n_pairs;
+};
+
+// Split k = 0..K-1 into launches whose channel pairs fit in shared memory
+// (k = 0 contributes one pair (f, 1), every k >= 1 two), balancing pair counts.
+std::vector<Chunk> plan_chunks(int K, int max_pairs) {
+    const int total = 2 * K - 1;
+    const int n_chunks = (total + max_pairs - 1) / max_pairs;
+    const int target = (total + n_chunks - 1) / n_chunks;
+    std::vector<Chunk> out;
+    int k = 0;
+    while (k < K) {
+        Chunk c{k, 0, 0};
+        while (k < K) {
+            const int add = k == 0 ? 1 : 2;
+            if (c.n_pairs + add > target && c.n_k > 0) break;
+            if (c.n_pairs + add > max_pairs) break;
+            c.n_pairs += add;
+            ++c.n_k;
+            ++k;
+        }
+        out.push_back(c);
+    }
+    return out;
+}
+
+struct Job {
+    const float* d_src;
+    long long src_frame_stride;
+    int src_row0, src_rows;
+    float* d_dst;
+    long long dst_frame_stride;
+    int width, height, n_frames;
+    int out_row0, out_rows;
+};
+
+// Runs every chunk launch for one job on `stream`. `scratch` must hold
+// n_frames * out_rows * width float2 when K needs more than one chunk.
+int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int border,
+            float2* scratch, unsigned long long* d_fallbacks, cudaStream_t stream) {
+    const int r = (int)std::ceil(3.0 * theta);
+    const auto& ent = fbf_dev::radius_entry(r);
+    const auto chunks = plan_chunks(a.K, ent.max_pairs);
+    if (chunks.size() > 1 && !scratch) return fail(FBF_EINVAL, "internal: scratch required");
+
+    fbf_dev::Params p{};
+    p.src = job.d_src;
+    p.src_frame_stride = job.src_frame_stride;
+    p.src_pitch = job.width;
+    p.src_row0 = job.src_row0;
+    p.src_rows = job.src_rows;
+    p.dst = job.d_dst;
+    p.dst_frame_stride = job.dst_frame_stride;
+    p.dst_pitch = job.width;
+    p.acc = chunks.size() > 1 ? scratch : nullptr;
+    p.acc_frame_stride = (long long)job.out_rows * job.width;
+    p.fallbacks = d_fallbacks;
+    p.width = job.width;
+    p.height = job.height;
+    p.n_frames = job.n_frames;
+    p.border = border;
+    p.out_row0 = job.out_row0;
+    p.out_rows = job.out_rows;
+    p.n_strips = (job.width + kTW - 1) / kTW;
+    p.total_units = (long long)job.n_frames * p.n_strips * job.out_rows;
+    // kernels.cpp:105-118 taps, kept by |d|
+    for (int j = 0; j <= r; ++j)
+        p.taps[j] = (float)std::exp(-((double)j * j) / (2.0 * theta * theta));
+    // each CTA should stream segments of at least a few steps
+    const long long min_seg = 2 * fbf_dev::kQ;
+    const long long want = (p.total_units + min_seg - 1) / min_seg;
+    const int grid = (int)std::max(1LL, std::min<long long>(ctx.num_sms, want));
+
+    for (size_t ci = 0; ci < chunks.size(); ++ci) {
+        const Chunk& c = chunks[ci];
+        p.k_lo = c.k_lo;
+        p.n_k = c.n_k;
+        p.n_pairs = c.n_pairs;
+        p.first_chunk = ci == 0;
+        p.last_chunk = ci + 1 == chunks.size();
+        for (int kk = 0; kk < c.n_k; ++kk) {
+            const int k = c.k_lo + kk;
+            p.coeff[kk] = (float)a.c[k];
+            p.kinv[kk] = (double)k / (2.0 * a.T + 1.0);
+        }
+        const cudaError_t e = ent.launch(p, grid, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "fbf_fused_kernel launch");
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    return FBF_OK;
+}
+
+size_t scratch_bytes(const Approx& a, double theta, size_t pixels) {
+    const int r = (int)std::ceil(3.0 * theta);
+    const auto& ent = fbf_dev::radius_entry(r);
+    return plan_chunks(a.K, ent.max_pairs).size() > 1 ? pixels * sizeof(float2) : 0;
+}
+
+size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+// Host-buffer path for n_frames frames on one device (H2D, validate, filter, D2H).
+int filter_frames_on_device(int dev, const float* img, int n_frames, int width, int height, double theta,
+                            const Approx& a, int border, float* out, long long* fallbacks) {
+    DeviceCtx* ctx = nullptr;
+    int rc = get_ctx(dev, &ctx);
+    if (rc != FBF_OK) return rc;
+    std::lock_guard<std::mutex> lock(ctx->mtx);
+    FBF_CUDA(cudaSetDevice(dev), "cudaSetDevice");
+    const size_t pixels = (size_t)n_frames * width * height;
+    const size_t img_bytes = align_up(pixels * sizeof(float));
+    const size_t scr = align_up(scratch_bytes(a, theta, pixels));
+    rc = ctx->reserve(2 * img_bytes + scr);
+    if (rc != FBF_OK) return rc;
+    float* d_in = (float*)ctx->arena;
+    float* d_out = (float*)((char*)ctx->arena + img_bytes);
+    float2* d_scr = scr ? (float2*)((char*)ctx->arena + 2 * img_bytes) : nullptr;
+    cudaStream_t st = ctx->stream;
+    FBF_CUDA(cudaMemsetAsync(ctx->d_counters, 0, 2 * sizeof(unsigned long long), st), "memset");
+    FBF_CUDA(cudaMemcpyAsync(d_in, img, pixels * sizeof(float), cudaMemcpyHostToDevice, st), "H2D");
+    fbf_dev::validate_kernel<<<ctx->num_sms * 4, 256, 0, st>>>(d_in, pixels, (float)a.R,
+                                                              (unsigned int*)(ctx->d_counters + 1));
+    FBF_CUDA(cudaGetLastError(), "validate launch");
+    Job job{d_in, (long long)width * height, 0, height, d_out, (long long)width * height,
+            width, height, n_frames, 0, height};
+    rc = run_job(*ctx, job, theta, a, border, d_scr, ctx->d_counters, st);
+    if (rc != FBF_OK) return rc;
+    FBF_CUDA(cudaMemcpyAsync(out, d_out, pixels * sizeof(float), cudaMemcpyDeviceToHost, st), "D2H");
+    FBF_CUDA(cudaMemcpyAsync(ctx->h_counters, ctx->d_counters, 2 * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, st), "D2H counters");
+    FBF_CUDA(cudaStreamSynchronize(st), "filter");
+    if (ctx->h_counters[1]) return fail(FBF_ERANGE, "filter: pixel intensity outside [0, R]");
+    if (fallbacks) *fallbacks += (long long)ctx->h_counters[0];
+    return FBF_OK;
+}
+
+int make_approx(int K, int T, int R, const double* coeffs, Approx& a) {
+    a.K = K;
+    a.T = T;
+    a.R = R;
+    a.c.assign(coeffs, coeffs + K);
+    for (double v : a.c)
+        if (!std::isfinite(v)) return fail(FBF_EINVAL, "fast_bilateral: non-finite coefficient");
+    return FBF_OK;
+}
+
+int resolve_gpus(int n_gpus, int* out) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(FBF_ECUDA, "no CUDA device available (the fbf filter has no CPU fallback)");
+    }
+    *out = n_gpus <= 0 ? n : std::min(n_gpus, n);
+    return FBF_OK;
+}
+
+// Runs fn(g) on one host thread per device and returns the first failure.
+template <typename Fn>
+int per_device(int G, Fn&& fn) {
+    std::vector<int> rcs(G, FBF_OK);
+    std::vector<std::string> msgs(G);
+    std::vector<std::thread> th;
+    for (int g = 0; g < G; ++g)
+        th.emplace_back([&, g] {
+            rcs[g] = fn(g);
+            if (rcs[g] != FBF_OK) msgs[g] = fbf_last_error();
+        });
+    for (auto& t : th) t.join();
+    for (int g = 0; g < G; ++g)
+        if (rcs[g] != FBF_OK) return fail(rcs[g], msgs[g]);
+    return FBF_OK;
+}
+
+void source_window(int height, int out_row0, int out_rows, int r, int border, int* row0, int* rows) {
+    int lo = std::max(0, out_row0 - r), hi = std::min(height, out_row0 + out_rows + r);
+    // halo rows outside the image reach back in through the border mapping
+    auto widen = [&](int y) {
+        if (y >= 0 && y < height) return;
+        const int m = fbf_dev::map_border(y, height, border);
+        if (m < 0) return;
+        lo = std::min(lo, m);
+        hi = std::max(hi, m + 1);
+    };
+    for (int y = out_row0 - r; y < out_row0; ++y) widen(y);
+    for (int y = out_row0 + out_rows; y < out_row0 + out_rows + r; ++y) widen(y);
+    *row0 = lo;
+    *rows = hi - lo;
+}
+
+}  // namespace
+}  // namespace fbf_b200
+
+using namespace fbf_b200;
+
+extern "C" {
+
+int fbf_set_device(int device) {
+    if (device < 0 || device >= fbf_device_count()) return fail(FBF_EINVAL, "device index out of range");
+    g_default_device.store(device);
+    return FBF_OK;
+}
+
+int fbf_get_device(void) { return g_default_device.load(); }
+
+unsigned long long fbf_kernel_launches(void) { return g_launches.load(); }
+
+int fbf_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int fbf_validate_f32_device(const float* d_img, size_t n, int R, int device, void* stream) {
+    DeviceCtx* ctx = nullptr;
+    int rc = get_ctx(device, &ctx);
+    if (rc != FBF_OK) return rc;
+    std::lock_guard<std::mutex> lock(ctx->mtx);
+    FBF_CUDA(cudaSetDevice(device), "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;  // NULL = the legacy default stream
+    FBF_CUDA(cudaMemsetAsync(ctx->d_counters + 1, 0, sizeof(unsigned long long), st), "memset");
+    fbf_dev::validate_kernel<<<ctx->num_sms * 4, 256, 0, st>>>(d_img, n, (float)R,
+                                                              (unsigned int*)(ctx->d_counters + 1));
+    FBF_CUDA(cudaGetLastError(), "validate launch");
+    FBF_CUDA(cudaMemcpyAsync(ctx->h_counters + 1, ctx->d_counters + 1, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, st), "D2H");
+    FBF_CUDA(cudaStreamSynchronize(st), "validate");
+    if (ctx->h_counters[1]) return fail(FBF_ERANGE, "filter: pixel intensity outside [0, R]");
+    return FBF_OK;
+}
+
+int fbf_fast_bilateral_f32(const float* img, int width, int height, double theta, int K, int T, int R,
+                           const double* coeffs, int border, float* out, long long* fallbacks) {
+    int r = 0;
+    int rc = check_args(width, height, theta, K, T, R, coeffs, border, &r);
+    if (rc != FBF_OK) return rc;
+    Approx a;
+    rc = make_approx(K, T, R, coeffs, a);
+    if (rc != FBF_OK) return rc;
+    rc = filter_frames_on_device(g_default_device.load(), img, 1, width, height, theta, a, border, out, fallbacks);
+    if (rc == FBF_OK) clear_error();
+    return rc;
+}
+
+int fbf_fast_bilateral_f32_device(const float* d_img, int width, int height, double theta, int K, int T,
+                                  int R, const double* coeffs, int border, float* d_out,
+                                  unsigned long long* d_fallbacks, int device, void* stream) {
+    return fbf_fast_bilateral_band_f32_device(d_img, 0, height, width, height, 0, height, theta, K, T, R,
+                                              coeffs, border, d_out, d_fallbacks, device, stream);
+}
+
+int fbf_fast_bilateral_band_f32_device(const float* d_src, int src_row0, int src_rows, int width, int height,
+                                       int out_row0, int out_rows, double theta, int K, int T, int R,
+                                       const double* coeffs, int border, float* d_dst,
+                                       unsigned long long* d_fallbacks, int device, void* stream) {
+    int r = 0;
+    int rc = check_args(width, height, theta, K, T, R, coeffs, border, &r);
+    if (rc != FBF_OK) return rc;
+    if (out_row0 < 0 || out_rows <= 0 || out_row0 + out_rows > height)
+        return fail(FBF_EINVAL, "band: output rows outside the image");
+    int need0 = 0, need_rows = 0;
+    source_window(height, out_row0, out_rows, r, border, &need0, &need_rows);
+    if (src_row0 > need0 || src_row0 + src_rows < need0 + need_rows)
+        return fail(FBF_EINVAL, "band: source rows do not cover the halo");
+    Approx a;
+    rc = make_approx(K, T, R, coeffs, a);
+    if (rc != FBF_OK) return rc;
+    DeviceCtx* ctx = nullptr;
+    rc = get_ctx(device, &ctx);
+    if (rc != FBF_OK) return rc;
+    std::lock_guard<std::mutex> lock(ctx->mtx);
+    FBF_CUDA(cudaSetDevice(device), "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;  // NULL = the legacy default stream
+    const size_t scr = scratch_bytes(a, theta, (size_t)out_rows * width);
+    float2* d_scr = nullptr;
+    if (scr) {
+        rc = ctx->reserve(scr);
+        if (rc != FBF_OK) return rc;
+        d_scr = (float2*)ctx->arena;
+    }
+    Job job{d_src, 0, src_row0, src_rows, d_dst, 0, width, height, 1, out_row0, out_rows};
+    rc = run_job(*ctx, job, theta, a, border, d_scr, d_fallbacks, st);
+    if (rc == FBF_OK) clear_error();
+    return rc;
+}
+
+int fbf_band_source_rows(int height, int out_row0, int out_rows, double theta, int border, int* row0,
+                         int* rows) {
+    if (!(theta > 0.0) || height <= 0 || out_rows <= 0 || out_row0 < 0 || out_row0 + out_rows > height)
+        return fail(FBF_EINVAL, "band: invalid arguments");
+    source_window(height, out_row0, out_rows, (int)std::ceil(3.0 * theta), border, row0, rows);
+    return FBF_OK;
+}
+
+int fbf_fast_bilateral_batch_f32(const float* img, int n_frames, int width, int height, double theta, int K,
+                                 int T, int R, const double* coeffs, int border, float* out,
+                                 long long* fallbacks, int n_gpus) {
+    int r = 0;
+    int rc = check_args(width, height, theta, K, T, R, coeffs, border, &r);
+    if (rc != FBF_OK) return rc;
+    if (n_frames <= 0) return fail(FBF_EINVAL, "batch: n_frames must be positive");
+    Approx a;
+    rc = make_approx(K, T, R, coeffs, a);
+    if (rc != FBF_OK) return rc;
+    int G = 0;
+    rc = resolve_gpus(n_gpus, &G);
+    if (rc != FBF_OK) return rc;
+    G = std::min(G, n_frames);
+    const size_t fp = (size_t)width * height;
+    std::vector<long long> fb(G, 0);
+    rc = per_device(G, [&](int g) {
+        const int f0 = (int)((long long)n_frames * g / G), f1 = (int)((long long)n_frames * (g + 1) / G);
+        return filter_frames_on_device(g, img + f0 * fp, f1 - f0, width, height, theta, a, border,
+                                       out + f0 * fp, &fb[g]);
+    });
+    if (rc != FBF_OK) return rc;
+    if (fallbacks)
+        for (long long v : fb) *fallbacks += v;
+    clear_error();
+    return FBF_OK;
+}
+
+int fbf_fast_bilateral_bands_f32(const float* img, int width, int height, double theta, int K, int T, int R,
+                                 const double* coeffs, int border, float* out, long long* fallbacks,
+                                 int n_gpus) {
+    int r = 0;
+    int rc = check_args(width, height, theta, K, T, R, coeffs, border, &r);
+    if (rc != FBF_OK) return rc;
+    Approx a;
+    rc = make_approx(K, T, R, coeffs, a);
+    if (rc != FBF_OK) return rc;
+    int G = 0;
+    rc = resolve_gpus(n_gpus, &G);
+    if (rc != FBF_OK) return rc;
+    G = std::max(1, std::min(G, height));
+    std::vector<long long> fb(G, 0);
+    rc = per_device(G, [&](int g) -> int {
+        const int y0 = (int)((long long)height * g / G), y1 = (int)((long long)height * (g + 1) / G);
+        int s0 = 0, sn = 0;
+        source_window(height, y0, y1 - y0, r, border, &s0, &sn);
+        DeviceCtx* ctx = nullptr;
+        int rc2 = get_ctx(g, &ctx);
+        if (rc2 != FBF_OK) return rc2;
+        std::lock_guard<std::mutex> lock(ctx->mtx);
+        FBF_CUDA(cudaSetDevice(g), "cudaSetDevice");
+        const size_t in_b = align_up((size_t)sn * width * sizeof(float));
+        const size_t out_b = align_up((size_t)(y1 - y0) * width * sizeof(float));
+        const size_t scr = align_up(scratch_bytes(a, theta, (size_t)(y1 - y0) * width));
+        rc2 = ctx->reserve(in_b + out_b + scr);
+        if (rc2 != FBF_OK) return rc2;
+        float* d_in = (float*)ctx->arena;
+        float* d_out = (float*)((char*)ctx->arena + in_b);
+        float2* d_scr = scr ? (float2*)((char*)ctx->arena + in_b + out_b) : nullptr;
+        cudaStream_t st = ctx->stream;
+        FBF_CUDA(cudaMemsetAsync(ctx->d_counters, 0, 2 * sizeof(unsigned long long), st), "memset");
+        FBF_CUDA(cudaMemcpyAsync(d_in, img + (size_t)s0 * width, (size_t)sn * width * sizeof(float),
+                                 cudaMemcpyHostToDevice, st), "H2D band");
+        fbf_dev::validate_kernel<<<ctx->num_sms * 4, 256, 0, st>>>(d_in, (size_t)sn * width, (float)a.R,
+                                                                  (unsigned int*)(ctx->d_counters + 1));
+        FBF_CUDA(cudaGetLastError(), "validate launch");
+        Job job{d_in, 0, s0, sn, d_out, 0, width, height, 1, y0, y1 - y0};
+        rc2 = run_job(*ctx, job, theta, a, border, d_scr, ctx->d_counters, st);
+        if (rc2 != FBF_OK) return rc2;
+        FBF_CUDA(cudaMemcpyAsync(out + (size_t)y0 * width, d_out, (size_t)(y1 - y0) * width * sizeof(float),
+                                 cudaMemcpyDeviceToHost, st), "D2H band");
+        FBF_CUDA(cudaMemcpyAsync(ctx->h_counters, ctx->d_counters, 2 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, st), "D2H counters");
+        FBF_CUDA(cudaStreamSynchronize(st), "bands");
+        if (ctx->h_counters[1]) return fail(FBF_ERANGE, "filter: pixel intensity outside [0, R]");
+        fb[g] = (long long)ctx->h_counters[0];
+        return FBF_OK;
+    });
+    if (rc != FBF_OK) return rc;
+    if (fallbacks)
+        for (long long v : fb) *fallbacks += v;
+    clear_error();
+    return FBF_OK;
+}
+
+int fbf_filter(const float* img, int height, int width, double theta, double sigma, double eps_or_K,
+               float* out) {
+    // run_filter (tools/fourierbf.cpp:236-270) with the CLI defaults: Gaussian
+    // kernel, R = 255, symmetric border
+    const int R = 255;
+    const bool is_K = eps_or_K >= 1.0 && std::floor(eps_or_K) == eps_or_K;
+    std::vector<double> c(2 * R + 1);
+    int K = 0, T = 0;
+    double err = 0.0;
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    int rc = fbf_select_params(FBF_KERNEL_GAUSSIAN, sigma, R, is_K ? 0.0 : eps_or_K, is_K ? (int)eps_or_K : 0, 0,
+                               0, hw, &K, &T, c.data(), (int)c.size(), &err);
+    if (rc != FBF_OK) return rc;
+    return fbf_fast_bilateral_f32(img, width, height, theta, K, T, R, c.data(), FBF_BORDER_SYMMETRIC, out,
+                                  nullptr);
+}
+
+}  // extern "C"

@@ -1,0 +1,501 @@
+"""Python mirror of the reference fourierbf filtering interface (namespace fbf).
+
+Same names, argument meaning and error behaviour as the reference C++ API, so
+callers (and the parity tests) read like the reference's own code:
+
+    kernel = build_spatial_kernel(5.0)                       # kernels.hpp:42-51
+    samples = sample_range_kernel(RangeKernelSpec.gaussian(50.0, 255))
+    approx = fit_fixed_period(samples, 4, 203)               # approx.hpp:61-64
+    out = fast_bilateral(img, kernel, approx, BorderPolicy.symmetric, diag)
+                                                             # filter.hpp:43-46
+
+Everything numeric goes through libfbf.so (include/fbf.h): the optimiser runs
+in C++ on the host, the filter runs the fused sm_100a kernel. There is no CPU
+fallback; without a GPU the filter raises CudaError.
+
+Error mapping (reference exception -> Python):
+    std::invalid_argument        -> InvalidArgument (a ValueError)
+    ToleranceUnreachable          -> ToleranceUnreachable (carries best_found)
+    CUDA failures                 -> CudaError
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import (FBF_ECAPACITY, FBF_ECUDA, FBF_EINVAL, FBF_ENOMEM, FBF_ERANGE, FBF_EUNREACHABLE,
+                   FBF_OK)
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_fp = ctypes.POINTER(ctypes.c_float)
+
+
+class FbfError(RuntimeError):
+    pass
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class CudaError(FbfError):
+    pass
+
+
+class ToleranceUnreachable(FbfError):
+    """approx.hpp:97-103 -- raised with the best fit found."""
+
+    def __init__(self, message: str, best_found: "OptimizationReport"):
+        super().__init__(message)
+        self.best_found = best_found
+
+
+def _check(rc: int) -> None:
+    if rc == FBF_OK:
+        return
+    msg = _lib.last_error()
+    if rc in (FBF_EINVAL, FBF_ERANGE):
+        raise InvalidArgument(msg)
+    if rc == FBF_ECUDA:
+        raise CudaError(msg)
+    if rc == FBF_ENOMEM:
+        raise MemoryError(msg)
+    if rc == FBF_ECAPACITY:
+        raise InvalidArgument(msg)
+    raise FbfError(f"fbf error {rc}: {msg}")
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def _fptr(a: np.ndarray):
+    return a.ctypes.data_as(_fp)
+
+
+class BorderPolicy(enum.IntEnum):
+    """image.hpp:38."""
+    symmetric = 0
+    replicate = 1
+    zero = 2
+
+
+def _border(b) -> int:
+    if isinstance(b, str):
+        return int(BorderPolicy[b])
+    return int(b)
+
+
+class RangeKernelKind(enum.IntEnum):
+    """kernels.hpp:8 (parametric kinds; tabulated kernels enter as samples)."""
+    gaussian = 0
+    exponential = 1
+    cauchy = 2
+
+
+@dataclass
+class RangeKernelSpec:
+    """kernels.hpp:13-22."""
+    kind: RangeKernelKind = RangeKernelKind.gaussian
+    sigma: float = 0.0
+    dynamic_range: int = 255
+
+    @staticmethod
+    def gaussian(sigma: float, dynamic_range: int = 255) -> "RangeKernelSpec":
+        return RangeKernelSpec(RangeKernelKind.gaussian, sigma, dynamic_range)
+
+    @staticmethod
+    def exponential(sigma: float, dynamic_range: int = 255) -> "RangeKernelSpec":
+        return RangeKernelSpec(RangeKernelKind.exponential, sigma, dynamic_range)
+
+    @staticmethod
+    def cauchy(sigma: float, dynamic_range: int = 255) -> "RangeKernelSpec":
+        return RangeKernelSpec(RangeKernelKind.cauchy, sigma, dynamic_range)
+
+
+@dataclass
+class RangeKernelSamples:
+    """kernels.hpp:26-33: values[t + R] = phi(t), t in -R..R."""
+    dynamic_range: int
+    values: np.ndarray
+
+    def at(self, t: int) -> float:
+        return float(self.values[t + self.dynamic_range])
+
+    def lattice_size(self) -> int:
+        return 2 * self.dynamic_range + 1
+
+
+def sample_range_kernel(spec: RangeKernelSpec) -> RangeKernelSamples:
+    """kernels.cpp:78-103."""
+    R = int(spec.dynamic_range)
+    v = np.zeros(2 * R + 1)
+    _check(_lib.load().fbf_sample_range_kernel(int(spec.kind), float(spec.sigma), R, _dptr(v)))
+    return RangeKernelSamples(R, v)
+
+
+def tabulated_samples(values) -> RangeKernelSamples:
+    """RangeKernelSpec::tabulated + sample_range_kernel (kernels.cpp:51-77, 86-95)."""
+    v = np.asarray(values, dtype=np.float64)
+    if v.size < 3 or v.size % 2 == 0:
+        raise InvalidArgument("tabulated kernel: need an odd number of samples (2R+1), R >= 1")
+    if not np.all(np.isfinite(v)):
+        raise InvalidArgument("tabulated kernel: non-finite sample")
+    R = v.size // 2
+    if not v[R] > 0:
+        raise InvalidArgument("tabulated kernel: center value must be positive")
+    lo, hi = v[:R][::-1], v[R + 1:]
+    if np.any(np.abs(lo - hi) > 1e-12):
+        raise InvalidArgument("tabulated kernel: samples asymmetric beyond 1e-12")
+    if np.any(lo > v[R]) or np.any(hi > v[R]):
+        raise InvalidArgument("tabulated kernel: center must be the maximum")
+    out = np.empty_like(v)
+    out[R:] = v[R:]
+    out[:R] = v[R + 1:][::-1]
+    return RangeKernelSamples(R, out)
+
+
+@dataclass
+class SpatialKernel:
+    """kernels.hpp:42-48."""
+    theta: float
+    radius: int
+    taps: np.ndarray
+
+    def tap(self, j: int) -> float:
+        return float(self.taps[j + self.radius])
+
+
+def build_spatial_kernel(theta: float) -> SpatialKernel:
+    """kernels.cpp:105-118: radius ceil(3 theta), unnormalised taps."""
+    cap = 2 * max(0, math.ceil(3.0 * theta)) + 1 if math.isfinite(theta) and theta > 0 else 1
+    taps = np.zeros(cap)
+    r = _lib.load().fbf_build_spatial_kernel(float(theta), _dptr(taps), cap)
+    if r < 0:
+        _check(-r)
+    return SpatialKernel(float(theta), r, taps)
+
+
+def frequency_of(half_period: int) -> float:
+    return 2.0 * math.pi / (2.0 * half_period + 1.0)
+
+
+@dataclass
+class FourierApproximation:
+    """approx.hpp:14-22: phihat(t) = sum_k c_k cos(nu k t), nu = 2 pi / (2T+1)."""
+    terms: int = 0
+    half_period: int = 0
+    dynamic_range: int = 0
+    frequency: float = 0.0
+    coefficients: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+    def evaluate(self, t: int) -> float:
+        """approx.cpp:34-42."""
+        base = self.frequency * abs(t)
+        s = 0.0
+        for k in range(self.terms):
+            s += float(self.coefficients[k]) * math.cos(base * k)
+        return s
+
+
+def tabulate_approximation(approx: FourierApproximation) -> RangeKernelSamples:
+    """approx.cpp:48-59."""
+    R = approx.dynamic_range
+    v = np.zeros(2 * R + 1)
+    for t in range(R + 1):
+        e = approx.evaluate(t)
+        v[R + t] = e
+        v[R - t] = e
+    return RangeKernelSamples(R, v)
+
+
+def _approx(K: int, T: int, R: int, c: np.ndarray) -> FourierApproximation:
+    return FourierApproximation(K, T, R, frequency_of(T), np.array(c[:K], dtype=np.float64))
+
+
+def fit_fixed_period(samples: RangeKernelSamples, terms: int, half_period: int) -> FourierApproximation:
+    """approx.cpp:105-117."""
+    c = np.zeros(max(1, terms))
+    err = ctypes.c_double(0)
+    _check(_lib.load().fbf_fit_fixed_period(_dptr(samples.values), samples.dynamic_range, terms,
+                                            half_period, _dptr(c), ctypes.byref(err)))
+    return _approx(terms, half_period, samples.dynamic_range, c)
+
+
+def fit_error(samples: RangeKernelSamples, terms: int, half_period: int) -> float:
+    """||A c - b||^2 of the fixed-period fit (FitResult::error, approx.hpp:37-40)."""
+    c = np.zeros(max(1, terms))
+    err = ctypes.c_double(0)
+    _check(_lib.load().fbf_fit_fixed_period(_dptr(samples.values), samples.dynamic_range, terms,
+                                            half_period, _dptr(c), ctypes.byref(err)))
+    return err.value
+
+
+def scan_period_errors(terms: int, samples: RangeKernelSamples, t_max: int, threads: int = 1) -> np.ndarray:
+    """approx.cpp:119-130: result[T-1] = E(K, T)."""
+    e = np.zeros(max(1, t_max))
+    _check(_lib.load().fbf_scan_period_errors(_dptr(samples.values), samples.dynamic_range, terms, t_max,
+                                              threads, _dptr(e)))
+    return e
+
+
+@dataclass
+class PeriodScanResult:
+    best_half_period: int
+    best_error: float
+
+
+def min_error_over_period(terms: int, samples: RangeKernelSamples, t_max: int,
+                          threads: int = 1) -> PeriodScanResult:
+    """approx.cpp:132-144."""
+    T = ctypes.c_int(0)
+    e = ctypes.c_double(0)
+    _check(_lib.load().fbf_min_error_over_period(_dptr(samples.values), samples.dynamic_range, terms, t_max,
+                                                 threads, ctypes.byref(T), ctypes.byref(e)))
+    return PeriodScanResult(T.value, e.value)
+
+
+@dataclass
+class PerOrderError:
+    terms: int
+    best_half_period: int
+    best_error: float
+
+
+@dataclass
+class OptimizeOptions:
+    """approx.hpp:90-95."""
+    t_max: int = 0
+    k_max: int = 0
+    threads: int = 1
+
+
+@dataclass
+class OptimizationReport:
+    """approx.hpp:74-88."""
+    best_terms: int
+    best_half_period: int
+    coefficients: np.ndarray
+    achieved_error: float
+    tolerance: float
+    t_max: int
+    per_order: list
+
+    def approximation(self, dynamic_range: int) -> FourierApproximation:
+        return _approx(self.best_terms, self.best_half_period, dynamic_range, self.coefficients)
+
+
+def optimize_parameters(samples: RangeKernelSamples, tolerance: float,
+                        options: OptimizeOptions | None = None) -> OptimizationReport:
+    """approx.cpp:179-240 (Algorithm 1)."""
+    o = options or OptimizeOptions()
+    R = samples.dynamic_range
+    t_max = o.t_max if o.t_max > 0 else 10 * R
+    k_cap = min(o.k_max if o.k_max > 0 else 2 * R + 1, t_max + 1)
+    cap = max(1, k_cap)
+    c = np.zeros(cap)
+    per = np.zeros(3 * cap)
+    K, T, n = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    e = ctypes.c_double(0)
+    rc = _lib.load().fbf_optimize_parameters(_dptr(samples.values), R, float(tolerance), o.t_max, o.k_max,
+                                             o.threads, ctypes.byref(K), ctypes.byref(T), _dptr(c), cap,
+                                             ctypes.byref(e), _dptr(per), ctypes.byref(n))
+    if rc not in (FBF_OK, FBF_EUNREACHABLE):
+        _check(rc)
+    orders = [PerOrderError(int(per[3 * i]), int(per[3 * i + 1]), float(per[3 * i + 2])) for i in range(n.value)]
+    rep = OptimizationReport(K.value, T.value, c[:K.value].copy(), e.value, float(tolerance), t_max, orders)
+    if rc == FBF_EUNREACHABLE:
+        raise ToleranceUnreachable(_lib.last_error(), rep)
+    return rep
+
+
+def select_parameters(sigma: float, *, eps: float | None = None, K: int | None = None, T: int | None = None,
+                      method: str = "fast", kernel: str = "gaussian", dynamic_range: int = 255,
+                      threads: int = 1) -> FourierApproximation:
+    """CLI select_parameters (tools/fourierbf.cpp:185-234)."""
+    R = dynamic_range
+    c = np.zeros(2 * R + 1)
+    Ko, To = ctypes.c_int(0), ctypes.c_int(0)
+    e = ctypes.c_double(0)
+    rc = _lib.load().fbf_select_params(int(RangeKernelKind[kernel]), float(sigma), R, float(eps or 0.0),
+                                       int(K or 0), int(T or 0), int(method == "fbf"), threads,
+                                       ctypes.byref(Ko), ctypes.byref(To), _dptr(c), c.size, ctypes.byref(e))
+    if rc == FBF_EUNREACHABLE:
+        rep = OptimizationReport(Ko.value, To.value, c[:Ko.value].copy(), e.value, float(eps or 0), 10 * R, [])
+        raise ToleranceUnreachable(_lib.last_error(), rep)
+    _check(rc)
+    return _approx(Ko.value, To.value, R, c)
+
+
+@dataclass
+class FilterDiagnostics:
+    """filter.hpp:15-17."""
+    fallback_pixels: int = 0
+
+
+def _as_image(img) -> np.ndarray:
+    a = np.asarray(img)
+    if a.ndim != 2:
+        raise InvalidArgument("GrayImage: expected a 2-D (height, width) array")
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _approx_args(approx: FourierApproximation):
+    if approx.terms < 1 or len(approx.coefficients) != approx.terms:
+        raise InvalidArgument("fast_bilateral: malformed approximation")
+    return np.ascontiguousarray(approx.coefficients, dtype=np.float64)
+
+
+def fast_bilateral(img, kernel: SpatialKernel, approx: FourierApproximation,
+                   border=BorderPolicy.symmetric, diag: FilterDiagnostics | None = None,
+                   out: np.ndarray | None = None) -> np.ndarray:
+    """filter.hpp:43-46 / filter.cpp:129-213 on the GPU (host buffers in, host buffer out).
+
+    `out` (optional) is a caller-owned float32 (H, W) C-contiguous array, e.g.
+    a view of pinned memory, written in place.
+    """
+    a = _as_image(img)
+    c = _approx_args(approx)
+    if out is None:
+        out = np.empty_like(a)
+    elif out.dtype != np.float32 or out.shape != a.shape or not out.flags.c_contiguous:
+        raise InvalidArgument("out must be a C-contiguous float32 array of the image shape")
+    fb = ctypes.c_longlong(0)
+    _check(_lib.load().fbf_fast_bilateral_f32(_fptr(a), a.shape[1], a.shape[0], kernel.theta, approx.terms,
+                                              approx.half_period, approx.dynamic_range, _dptr(c), _border(border),
+                                              _fptr(out), ctypes.byref(fb)))
+    if diag is not None:
+        diag.fallback_pixels += fb.value
+    return out
+
+
+def fast_bilateral_batch(frames, kernel: SpatialKernel, approx: FourierApproximation,
+                         border=BorderPolicy.symmetric, diag: FilterDiagnostics | None = None,
+                         n_gpus: int = 0) -> np.ndarray:
+    """Independent frames (n, height, width), sharded over n_gpus devices (0 = all)."""
+    a = np.ascontiguousarray(np.asarray(frames), dtype=np.float32)
+    if a.ndim != 3:
+        raise InvalidArgument("batch: expected (n_frames, height, width)")
+    c = _approx_args(approx)
+    out = np.empty_like(a)
+    fb = ctypes.c_longlong(0)
+    _check(_lib.load().fbf_fast_bilateral_batch_f32(_fptr(a), a.shape[0], a.shape[2], a.shape[1], kernel.theta,
+                                                    approx.terms, approx.half_period, approx.dynamic_range,
+                                                    _dptr(c), _border(border), _fptr(out), ctypes.byref(fb),
+                                                    n_gpus))
+    if diag is not None:
+        diag.fallback_pixels += fb.value
+    return out
+
+
+def fast_bilateral_bands(img, kernel: SpatialKernel, approx: FourierApproximation,
+                         border=BorderPolicy.symmetric, diag: FilterDiagnostics | None = None,
+                         n_gpus: int = 0) -> np.ndarray:
+    """One image split into row bands with replicated halos over n_gpus devices."""
+    a = _as_image(img)
+    c = _approx_args(approx)
+    out = np.empty_like(a)
+    fb = ctypes.c_longlong(0)
+    _check(_lib.load().fbf_fast_bilateral_bands_f32(_fptr(a), a.shape[1], a.shape[0], kernel.theta, approx.terms,
+                                                    approx.half_period, approx.dynamic_range, _dptr(c),
+                                                    _border(border), _fptr(out), ctypes.byref(fb), n_gpus))
+    if diag is not None:
+        diag.fallback_pixels += fb.value
+    return out
+
+
+def band_source_rows(height: int, out_row0: int, out_rows: int, theta: float,
+                     border=BorderPolicy.symmetric) -> tuple[int, int]:
+    """Global source-row window [row0, row0 + rows) a band needs (halo included)."""
+    r0, n = ctypes.c_int(0), ctypes.c_int(0)
+    _check(_lib.load().fbf_band_source_rows(height, out_row0, out_rows, float(theta), _border(border),
+                                            ctypes.byref(r0), ctypes.byref(n)))
+    return r0.value, n.value
+
+
+def fast_bilateral_device(d_img, kernel: SpatialKernel, approx: FourierApproximation, d_out,
+                          border=BorderPolicy.symmetric, d_fallbacks=None, stream=None) -> None:
+    """Device-resident variant on torch CUDA tensors (float32, contiguous, (H, W)).
+
+    Enqueued on `stream` (a torch.cuda.Stream; default: torch's current stream)
+    without synchronising. No intensity validation (see validate_device).
+    """
+    import torch
+    if d_img.dtype != torch.float32 or not d_img.is_cuda or not d_img.is_contiguous():
+        raise InvalidArgument("device image must be a contiguous float32 CUDA tensor")
+    H, W = d_img.shape
+    c = _approx_args(approx)
+    st = stream if stream is not None else torch.cuda.current_stream(d_img.device)
+    _check(_lib.load().fbf_fast_bilateral_f32_device(
+        ctypes.c_void_p(d_img.data_ptr()), W, H, kernel.theta, approx.terms, approx.half_period,
+        approx.dynamic_range, _dptr(c), _border(border), ctypes.c_void_p(d_out.data_ptr()),
+        ctypes.c_void_p(d_fallbacks.data_ptr() if d_fallbacks is not None else 0), d_img.device.index,
+        ctypes.c_void_p(st.cuda_stream)))
+
+
+def fast_bilateral_band_device(d_src, src_row0: int, height: int, out_row0: int, out_rows: int,
+                               kernel: SpatialKernel, approx: FourierApproximation, d_dst,
+                               border=BorderPolicy.symmetric, d_fallbacks=None, stream=None) -> None:
+    """One rank's band: d_src holds global rows [src_row0, src_row0 + d_src.shape[0])."""
+    import torch
+    rows, W = d_src.shape
+    c = _approx_args(approx)
+    st = stream if stream is not None else torch.cuda.current_stream(d_src.device)
+    _check(_lib.load().fbf_fast_bilateral_band_f32_device(
+        ctypes.c_void_p(d_src.data_ptr()), src_row0, rows, W, height, out_row0, out_rows, kernel.theta,
+        approx.terms, approx.half_period, approx.dynamic_range, _dptr(c), _border(border),
+        ctypes.c_void_p(d_dst.data_ptr()),
+        ctypes.c_void_p(d_fallbacks.data_ptr() if d_fallbacks is not None else 0), d_src.device.index,
+        ctypes.c_void_p(st.cuda_stream)))
+
+
+def validate_device(d_img, dynamic_range: int = 255, stream=None) -> None:
+    """validate_intensities (filter.cpp:19-23) on a device tensor."""
+    import torch
+    st = stream if stream is not None else torch.cuda.current_stream(d_img.device)
+    _check(_lib.load().fbf_validate_f32_device(ctypes.c_void_p(d_img.data_ptr()), d_img.numel(), dynamic_range,
+                                               d_img.device.index, ctypes.c_void_p(st.cuda_stream)))
+
+
+def fbf_filter(img, theta: float, sigma: float, eps_or_K: float) -> np.ndarray:
+    """North-star convenience call fbf_filter(img, H, W, theta, sigma, eps/K, out)."""
+    a = _as_image(img)
+    out = np.empty_like(a)
+    _check(_lib.load().fbf_filter(_fptr(a), a.shape[0], a.shape[1], float(theta), float(sigma), float(eps_or_K),
+                                  _fptr(out)))
+    return out
+
+
+# ---- synthetic inputs (synthetic.cpp + BASELINE.json generators) ----------
+
+def random_image(width: int, height: int, seed: int) -> np.ndarray:
+    out = np.empty((height, width), dtype=np.float32)
+    _lib.load().fbf_random_image_f32(width, height, seed, _fptr(out))
+    return out
+
+
+def scene_image(width: int, height: int, seed: int) -> np.ndarray:
+    out = np.empty((height, width), dtype=np.float32)
+    _lib.load().fbf_scene_image_f32(width, height, seed, _fptr(out))
+    return out
+
+
+def voronoi_image(width: int, height: int, n_sites: int, noise: float, seed: int, threads: int = 0) -> np.ndarray:
+    import os
+    out = np.empty((height, width), dtype=np.float32)
+    _lib.load().fbf_voronoi_image_f32(width, height, n_sites, noise, seed, threads or os.cpu_count() or 1,
+                                      _fptr(out))
+    return out
+
+
+def field_image(width: int, height: int, n_sites: int, noise: float, seed: int, threads: int = 0) -> np.ndarray:
+    import os
+    out = np.empty((height, width), dtype=np.float32)
+    _lib.load().fbf_field_image_f32(width, height, n_sites, noise, seed, threads or os.cpu_count() or 1,
+                                    _fptr(out))
+    return out
