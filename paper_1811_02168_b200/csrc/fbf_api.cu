@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <atomic>
@@ -27,7 +29,10 @@
 #include "fbf_kernel.cuh"
 
 namespace fbf_dev {
-#define FBF_EXTERN(R) extern template cudaError_t launch_fused<R>(const Params&, int, cudaStream_t);
+#define FBF_EXTERN1(R, N) \
+    extern template cudaError_t launch_fused<R, N>(const Params&, int, cudaStream_t);
+#define FBF_EXTERN(R) \
+    FBF_EXTERN1(R, 0) FBF_EXTERN1(R, 1) FBF_EXTERN1(R, 2) FBF_EXTERN1(R, 3) FBF_EXTERN1(R, 4) FBF_EXTERN1(R, 5)
 FBF_EXTERN(1) FBF_EXTERN(2) FBF_EXTERN(3) FBF_EXTERN(4) FBF_EXTERN(5) FBF_EXTERN(6) FBF_EXTERN(7)
 FBF_EXTERN(8) FBF_EXTERN(9) FBF_EXTERN(10) FBF_EXTERN(11) FBF_EXTERN(12) FBF_EXTERN(13)
 FBF_EXTERN(14) FBF_EXTERN(15) FBF_EXTERN(16) FBF_EXTERN(17) FBF_EXTERN(18) FBF_EXTERN(19)
@@ -35,24 +40,32 @@ FBF_EXTERN(20) FBF_EXTERN(21) FBF_EXTERN(22) FBF_EXTERN(23) FBF_EXTERN(24) FBF_E
 FBF_EXTERN(26) FBF_EXTERN(27) FBF_EXTERN(28) FBF_EXTERN(29) FBF_EXTERN(30) FBF_EXTERN(31)
 FBF_EXTERN(32)
 #undef FBF_EXTERN
+#undef FBF_EXTERN1
 
 namespace {
 
 using LaunchFn = cudaError_t (*)(const Params&, int, cudaStream_t);
 struct RadiusEntry {
-    LaunchFn launch;
-    int max_pairs;
+    LaunchFn launch[kMaxKR + 1];  // by NKR (number of k >= 1 terms in the launch)
+    int max_pairs[3];             // by CTAs per SM (index 1, 2)
+    int fsw;                      // TMA box width
     size_t pair_bytes, fixed_bytes;
 };
 
 template <int R>
 RadiusEntry entry() {
-    return {&launch_fused<R>, Geometry<R>::max_pairs(), Geometry<R>::pair_bytes, Geometry<R>::fixed_bytes};
+    using G = Geometry<R>;
+    return {{&launch_fused<R, 0>, &launch_fused<R, 1>, &launch_fused<R, 2>, &launch_fused<R, 3>,
+             &launch_fused<R, 4>, &launch_fused<R, 5>},
+            {0, G::max_pairs(1), G::max_pairs(2)},
+            G::FSW,
+            G::pair_bytes,
+            G::fixed_bytes};
 }
 
 const RadiusEntry& radius_entry(int r) {
     static const RadiusEntry table[kMaxRadius + 1] = {
-        {nullptr, 0, 0, 0}, entry<1>(),  entry<2>(),  entry<3>(),  entry<4>(),  entry<5>(),
+        RadiusEntry{}, entry<1>(),  entry<2>(),  entry<3>(),  entry<4>(),  entry<5>(),
         entry<6>(),  entry<7>(),  entry<8>(),  entry<9>(),  entry<10>(), entry<11>(),
         entry<12>(), entry<13>(), entry<14>(), entry<15>(), entry<16>(), entry<17>(),
         entry<18>(), entry<19>(), entry<20>(), entry<21>(), entry<22>(), entry<23>(),
@@ -172,20 +185,28 @@ struct Chunk {
     int k_lo, n_k, n_pairs;
 };
 
+struct Plan {
+    std::vector<Chunk> chunks;
+    int blocks_per_sm = 1;
+};
+
 // Split k = 0..K-1 into launches whose channel pairs fit in shared memory
-// (k = 0 contributes one pair (f, 1), every k >= 1 two), balancing pair counts.
-std::vector<Chunk> plan_chunks(int K, int max_pairs) {
+// (k = 0 contributes one pair (f, 1), every k >= 1 two; at most kMaxKR terms
+// k >= 1 per launch), balancing pair counts.
+std::vector<Chunk> split_chunks(int K, int max_pairs) {
+    std::vector<Chunk> out;
+    if (max_pairs < 2) max_pairs = 2;  // always room for one k >= 1 term
     const int total = 2 * K - 1;
     const int n_chunks = (total + max_pairs - 1) / max_pairs;
     const int target = (total + n_chunks - 1) / n_chunks;
-    std::vector<Chunk> out;
     int k = 0;
     while (k < K) {
         Chunk c{k, 0, 0};
         while (k < K) {
             const int add = k == 0 ? 1 : 2;
-            if (c.n_pairs + add > target && c.n_k > 0) break;
-            if (c.n_pairs + add > max_pairs) break;
+            const int nkr = c.n_k - (c.k_lo == 0 ? 1 : 0) + (k == 0 ? 0 : 1);
+            if (c.n_k > 0 && (c.n_pairs + add > target || c.n_pairs + add > max_pairs || nkr > fbf_dev::kMaxKR))
+                break;
             c.n_pairs += add;
             ++c.n_k;
             ++k;
@@ -193,6 +214,23 @@ std::vector<Chunk> plan_chunks(int K, int max_pairs) {
         out.push_back(c);
     }
     return out;
+}
+
+// Two CTAs per SM hide each other's barrier and generation phases; use them
+// unless that needs more coefficient chunks (each chunk re-streams the image).
+// FBF_BLOCKS_PER_SM=1|2 overrides (tuning).
+Plan make_plan(int K, int r) {
+    const auto& ent = fbf_dev::radius_entry(r);
+    Plan p1{split_chunks(K, ent.max_pairs[1]), 1};
+    Plan p2{split_chunks(K, ent.max_pairs[2]), 2};
+    static const int forced = [] {
+        const char* e = std::getenv("FBF_BLOCKS_PER_SM");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced == 1) return p1;
+    if (forced == 2 && ent.max_pairs[2] >= 2) return p2;
+    if (ent.max_pairs[2] >= 2 && p2.chunks.size() <= p1.chunks.size()) return p2;
+    return p1;
 }
 
 struct Job {
@@ -211,8 +249,8 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
             float2* scratch, unsigned long long* d_fallbacks, cudaStream_t stream) {
     const int r = (int)std::ceil(3.0 * theta);
     const auto& ent = fbf_dev::radius_entry(r);
-    const auto chunks = plan_chunks(a.K, ent.max_pairs);
-    if (chunks.size() > 1 && !scratch) return fail(FBF_EINVAL, "internal: scratch required");
+    const Plan plan = make_plan(a.K, r);
+    if (plan.chunks.size() > 1 && !scratch) return fail(FBF_EINVAL, "internal: scratch required");
 
     fbf_dev::Params p{};
     p.src = job.d_src;
@@ -223,7 +261,7 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
     p.dst = job.d_dst;
     p.dst_frame_stride = job.dst_frame_stride;
     p.dst_pitch = job.width;
-    p.acc = chunks.size() > 1 ? scratch : nullptr;
+    p.acc = plan.chunks.size() > 1 ? scratch : nullptr;
     p.acc_frame_stride = (long long)job.out_rows * job.width;
     p.fallbacks = d_fallbacks;
     p.width = job.width;
@@ -237,24 +275,27 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
     // kernels.cpp:105-118 taps, kept by |d|
     for (int j = 0; j <= r; ++j)
         p.taps[j] = (float)std::exp(-((double)j * j) / (2.0 * theta * theta));
-    // each CTA should stream segments of at least a few steps
-    const long long min_seg = 2 * fbf_dev::kQ;
+    // interior row spans go through the TMA bulk-copy engine when rows are 16-byte aligned
+    static const bool no_tma = std::getenv("FBF_NO_TMA") != nullptr;
+    p.use_tma = !no_tma && job.width % 4 == 0 && ((uintptr_t)job.d_src & 15) == 0 &&
+                (job.n_frames == 1 || job.src_frame_stride % 4 == 0);
+    // persistent grid: CTAs per SM x SMs, but keep segments at least a few steps long
+    const long long min_seg = 4 * fbf_dev::kQ;
     const long long want = (p.total_units + min_seg - 1) / min_seg;
-    const int grid = (int)std::max(1LL, std::min<long long>(ctx.num_sms, want));
+    const int grid = (int)std::max(1LL, std::min<long long>((long long)ctx.num_sms * plan.blocks_per_sm, want));
 
-    for (size_t ci = 0; ci < chunks.size(); ++ci) {
-        const Chunk& c = chunks[ci];
+    for (size_t ci = 0; ci < plan.chunks.size(); ++ci) {
+        const Chunk& c = plan.chunks[ci];
+        const int zk = c.k_lo == 0 ? 1 : 0;
+        const int nkr = c.n_k - zk;
         p.k_lo = c.k_lo;
-        p.n_k = c.n_k;
         p.n_pairs = c.n_pairs;
         p.first_chunk = ci == 0;
-        p.last_chunk = ci + 1 == chunks.size();
-        for (int kk = 0; kk < c.n_k; ++kk) {
-            const int k = c.k_lo + kk;
-            p.coeff[kk] = (float)a.c[k];
-            p.kinv[kk] = (double)k / (2.0 * a.T + 1.0);
-        }
-        const cudaError_t e = ent.launch(p, grid, stream);
+        p.last_chunk = ci + 1 == plan.chunks.size();
+        for (int kk = 0; kk < c.n_k; ++kk) p.coeff[kk] = (float)a.c[c.k_lo + kk];
+        p.kinv1 = 1.0 / (2.0 * a.T + 1.0);
+        p.kinv_first = (double)std::max(c.k_lo, 1) / (2.0 * a.T + 1.0);
+        const cudaError_t e = ent.launch[nkr](p, grid, stream);
         if (e != cudaSuccess) return cuda_fail(e, "fbf_fused_kernel launch");
         g_launches.fetch_add(1, std::memory_order_relaxed);
     }
@@ -263,8 +304,7 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
 
 size_t scratch_bytes(const Approx& a, double theta, size_t pixels) {
     const int r = (int)std::ceil(3.0 * theta);
-    const auto& ent = fbf_dev::radius_entry(r);
-    return plan_chunks(a.K, ent.max_pairs).size() > 1 ? pixels * sizeof(float2) : 0;
+    return make_plan(a.K, r).chunks.size() > 1 ? pixels * sizeof(float2) : 0;
 }
 
 size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }

@@ -9,18 +9,24 @@
 //   combine + fallback                    (src/filter.cpp:197-211)
 // without materialising any of the 4K-2 auxiliary images in HBM.
 //
-// Dataflow (one persistent CTA per SM, column strips streamed top to bottom):
+// Dataflow (persistent CTAs, 1-2 per SM, column strips streamed top to bottom):
 //   * The image is cut into strips of TW=32 output columns. Each CTA owns a
-//     contiguous range of (frame, strip, row) units, i.e. one or a few strip
-//     segments, so every SM gets the same number of output rows.
-//   * A segment is streamed in steps of Q=16 input rows. Per step:
-//       gen  : f for the Q new rows x (TW + 2r) columns (border-mapped), and
-//              the channel pairs (f, 1) for k = 0 and (C_k f, S_k f), (C_k, S_k)
-//              for k >= 1, C_k + i S_k = exp(i k nu f), into shared memory.
-//       row  : horizontal (2r+1)-tap pass of every channel pair, P=8 outputs
-//              per thread, packed FFMA2 with the tap broadcast from a uniform
-//              register; results go to a ring of Q + 2r rows.
-//       col  : vertical pass over the ring, P=8 outputs per thread, FFMA2.
+//     contiguous range of (frame, strip, row) units -- one or a few strip
+//     segments -- so every CTA gets the same number of output rows.
+//   * A segment is streamed in steps of Q=8 input rows. Per step:
+//       stage: the f tile of the NEXT step (Q rows x (TW+2r) columns) is
+//              fetched asynchronously: one TMA bulk copy per row
+//              (cp.async.bulk, mbarrier complete_tx) for interior tiles,
+//              border-mapped per-pixel cp.async at the image edges (the copy
+//              engine cannot mirror).
+//       gen  : channel pairs (f, 1) for k = 0 and (C_k f, S_k f), (C_k, S_k)
+//              for k >= 1, with C_k + i S_k = exp(i k nu f) from one
+//              double-reduced MUFU sincos and the angle-addition recurrence.
+//       row  : horizontal (2r+1)-tap pass of every channel pair, 8 outputs
+//              per thread, FFMA2 with the tap broadcast from a uniform
+//              register; results go to a ring of 1 + ceil(2r/Q) row blocks.
+//       col  : vertical pass over the ring, 8 outputs per thread, FFMA2; the
+//              ring window resolves to fixed offsets at compile time.
 //       comb : per output pixel, num += c_k (C_k G(C_k f) + S_k G(S_k f)),
 //              den += c_k (C_k G(C_k) + S_k G(S_k)) in ascending k, then
 //              out = den > 1e-12 ? num / den : f.
@@ -37,13 +43,17 @@
 namespace fbf_dev {
 
 constexpr int kTW = 32;          // output columns per strip
-constexpr int kQ = 16;           // input rows per pipeline step
+constexpr int kQ = 8;            // input rows per pipeline step
 constexpr int kP = 8;            // outputs per thread item (row and column passes)
-constexpr int kMaxPairs = 10;    // channel pairs per launch (block = 64 * pairs threads)
-constexpr int kMaxKC = kMaxPairs / 2 + 1;  // k values per launch
+constexpr int kMaxKR = 5;        // k >= 1 terms per launch (template parameter NKR <= kMaxKR)
+constexpr int kMaxPairs = 1 + 2 * kMaxKR;
 constexpr int kMaxRadius = 32;
-constexpr int kItemsPerPair = kQ * kTW / kP;  // 64 threads per channel pair
+constexpr int kItemsPerPair = kQ * kTW / kP;  // 32 threads (one warp) per channel pair
 constexpr size_t kSmemLimit = 232448;          // 227 KB opt-in per block on sm_100
+constexpr size_t kSmemPerSM = 233472;          // 228 KB per SM
+constexpr size_t kSmemReservedPerBlock = 1024;
+
+static_assert(kQ == kP, "one column-pass row group per step");
 
 struct Params {
     const float* src;            // frame 0, global row src_row0, column 0
@@ -58,26 +68,37 @@ struct Params {
     unsigned long long* fallbacks;  // device counter (may be null)
     int width, height, n_frames, border;
     int out_row0, out_rows;
-    int k_lo, n_k, n_pairs;
+    int k_lo, n_pairs;           // chunk: k in [k_lo, k_lo + (k_lo == 0) + NKR)
     int first_chunk, last_chunk;
     int n_strips;
-    long long total_units;  // n_frames * n_strips * out_rows
+    int use_tma;
+    long long total_units;       // n_frames * n_strips * out_rows
     float taps[kMaxRadius + 1];  // taps[j] = exp(-j^2 / (2 theta^2)), j = |d|
-    float coeff[kMaxKC];
-    double kinv[kMaxKC];         // k / (2T + 1) for the chunk's k values
+    float coeff[kMaxKR + 1];     // c_k of the chunk, ascending k
+    double kinv1;                // 1 / (2T + 1)
+    double kinv_first;           // max(k_lo, 1) / (2T + 1)
 };
 
 template <int R>
 struct Geometry {
     static constexpr int GW = kTW + 2 * R;                       // gen row width (pixels)
-    static constexpr int GS = GW + ((2 - GW % 4) + 4) % 4;       // stride, GS/2 odd
-    static constexpr int RING = kQ + 2 * R;                      // ring rows
-    static constexpr int RS = kTW + 2;                           // ring stride, RS/2 odd
-    static constexpr size_t pair_bytes = sizeof(float2) * (size_t)(kQ * GS + RING * RS);
-    static constexpr size_t fixed_bytes = sizeof(float) * (size_t)(RING * kTW) + 16;
+    static constexpr int GS = GW + ((2 - GW % 4) + 4) % 4;       // gen stride (float2), GS/2 odd
+    static constexpr int FSW = (GW + 3 + 3) / 4 * 4;             // f staging row: GW + 16B-alignment slack
+    static constexpr int RB = 1 + (2 * R + kQ - 1) / kQ;         // ring blocks of kQ rows
+    static constexpr int RROWS = RB * kQ;                        // ring rows
+    static constexpr int RS = kTW + 2;                           // ring stride (float2), RS/2 odd
+    static constexpr size_t fstage_bytes = sizeof(float) * 2 * kQ * FSW;  // multiple of 128
+    static constexpr size_t misc_bytes = 64;                              // 2 mbarriers + counter
+    static constexpr size_t colmap_bytes = sizeof(int) * ((GW + 3) / 4 * 4);
+    static constexpr size_t fring_bytes = sizeof(float) * RROWS * kTW;
+    static constexpr size_t fixed_bytes = fstage_bytes + misc_bytes + colmap_bytes + fring_bytes;
+    static constexpr size_t pair_bytes = sizeof(float2) * (size_t)(kQ * GS + RROWS * RS);
     static size_t smem_bytes(int pairs) { return fixed_bytes + pair_bytes * pairs; }
-    static int max_pairs() {
-        const size_t p = (kSmemLimit - fixed_bytes) / pair_bytes;
+    static int max_pairs(int blocks_per_sm) {
+        size_t budget = kSmemPerSM / blocks_per_sm - kSmemReservedPerBlock;
+        if (budget > kSmemLimit) budget = kSmemLimit;
+        if (budget <= fixed_bytes) return 0;
+        const size_t p = (budget - fixed_bytes) / pair_bytes;
         return (int)(p < (size_t)kMaxPairs ? p : (size_t)kMaxPairs);
     }
 };
@@ -93,9 +114,8 @@ __host__ __device__ __forceinline__ int map_border(int i, int n, int border) {
     return m < n ? m : period - 1 - m;
 }
 
-// (cos, sin)(2 pi * k f / (2T+1)): exact turn reduction in double, then the
-// MUFU pair on [-pi, pi]. Used identically by gen and combine, so the
-// modulation and demodulation factors agree bit for bit.
+// (cos, sin)(2 pi * kinv * f) with kinv = k / (2T+1): exact turn reduction in
+// double, then the MUFU pair on [-pi, pi].
 __device__ __forceinline__ float2 harmonic(float f, double kinv) {
     double t = (double)f * kinv;
     t -= rint(t);
@@ -105,25 +125,115 @@ __device__ __forceinline__ float2 harmonic(float f, double kinv) {
     return make_float2(c, s);
 }
 
+// exp(i (k+1) w) = exp(i k w) * exp(i w). gen and combine run this identical
+// sequence, so modulation and demodulation factors agree bit for bit.
+__device__ __forceinline__ float2 rotate(float2 cs, float2 c1) {
+    return make_float2(fmaf(cs.x, c1.x, -(cs.y * c1.y)), fmaf(cs.y, c1.x, cs.x * c1.y));
+}
+
 __device__ __forceinline__ float2 ffma2(float2 a, float w, float2 c) {
     return __ffma2_rn(a, make_float2(w, w), c);
 }
 
+// ---- async copy primitives ----------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+// 1-D TMA bulk copy global -> shared (16-byte aligned, size multiple of 16),
+// completion on `bar`.
+__device__ __forceinline__ void tma_bulk_g2s(float* smem_dst, const float* gsrc, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(smem_dst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// Vertical pass for the kQ output rows of the current step. The window rows
+// j in [-2R, kP) (relative to the newest ring block) resolve to (block, row)
+// at compile time, so every load is a fixed offset from one of RB per-step
+// block pointers.
 template <int R>
-__global__ void __launch_bounds__(kMaxPairs * kItemsPerPair, 1) fbf_fused_kernel(const Params p) {
+__device__ __forceinline__ void column_pass(const float2* __restrict__ ring_pair, int blk, int x,
+                                            const float* taps, float2* out_col) {
     using G = Geometry<R>;
-    constexpr int GW = G::GW, GS = G::GS, RING = G::RING, RS = G::RS;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int RB = G::RB, RS = G::RS;
+    const float2* bptr[RB];
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {  // bptr[b] = block (blk - b)
+        int bb = blk - b;
+        bb += bb < 0 ? RB : 0;
+        bptr[b] = ring_pair + bb * kQ * RS + x;
+    }
+    float2 acc[kP];
+#pragma unroll
+    for (int o = 0; o < kP; ++o) acc[o] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < kP + 2 * R; ++i) {
+        const int j = i - 2 * R;                          // compile-time
+        const int b = j >= 0 ? 0 : (-j + kQ - 1) / kQ;    // blocks back
+        const float2 v = bptr[b][(j + b * kQ) * RS];
+#pragma unroll
+        for (int o = 0; o < kP; ++o) {
+            const int d = i - o;
+            if (d >= 0 && d <= 2 * R) acc[o] = ffma2(v, taps[d >= R ? d - R : R - d], acc[o]);
+        }
+    }
+#pragma unroll
+    for (int o = 0; o < kP; ++o) out_col[o * kTW] = acc[o];
+}
+
+template <int R, int NKR>
+__global__ void __launch_bounds__(kMaxPairs * kItemsPerPair, 1)
+    fbf_fused_kernel(const __grid_constant__ Params p) {
+    using G = Geometry<R>;
+    constexpr int GW = G::GW, GS = G::GS, FSW = G::FSW, RB = G::RB, RROWS = G::RROWS, RS = G::RS;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int np = p.n_pairs;
-    float2* gen = reinterpret_cast<float2*>(smem_raw);       // [np][Q][GS]; later colout [np][Q][TW]
-    float2* ring = gen + (size_t)np * kQ * GS;                // [np][RING][RS]
-    float* fring = reinterpret_cast<float*>(ring + (size_t)np * RING * RS);  // [RING][TW]
-    unsigned int* s_fallbacks = reinterpret_cast<unsigned int*>(fring + RING * kTW);
+    float* fstage = reinterpret_cast<float*>(smem_raw);                    // [2][Q][FSW]
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw + G::fstage_bytes);  // [2]
+    unsigned int* s_fallbacks = reinterpret_cast<unsigned int*>(mbar + 2);
+    int* colmap = reinterpret_cast<int*>(smem_raw + G::fstage_bytes + G::misc_bytes);  // [GW]
+    float* fring = reinterpret_cast<float*>(smem_raw + G::fstage_bytes + G::misc_bytes + G::colmap_bytes);
+    float2* gen = reinterpret_cast<float2*>(fring + RROWS * kTW);           // [np][Q][GS]; colout [np][Q][TW]
+    float2* ring = gen + (size_t)np * kQ * GS;                              // [np][RROWS][RS]
     float2* colout = gen;
 
     const int tid = threadIdx.x;
     const int nthreads = blockDim.x;
-    if (tid == 0) *s_fallbacks = 0u;
+    const int zk = p.k_lo == 0 ? 1 : 0;  // k = 0 contributes the single pair (f, 1)
+    if (tid == 0) {
+        *s_fallbacks = 0u;
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    unsigned phase0 = 0, phase1 = 0;  // parity of the next completion of mbar[0/1]
 
     // this CTA's contiguous share of the (frame, strip, row) units
     const long long U = p.total_units;
@@ -144,6 +254,9 @@ __global__ void __launch_bounds__(kMaxPairs * kItemsPerPair, 1) fbf_fused_kernel
         const float* src = p.src + (long long)frame * p.src_frame_stride;
         float* dst = p.dst + (long long)frame * p.dst_frame_stride;
         float2* acc = p.acc ? p.acc + (long long)frame * p.acc_frame_stride : nullptr;
+        // interior strips copy 16-byte-aligned row spans [xs, xs + FSW) with the copy engine
+        const int xs = (x0 - R) & ~3, xoff = (x0 - R) - xs;
+        const bool cols_interior = p.use_tma && xs >= 0 && xs + FSW <= p.width;
 
         // steps start e rows early so that output rows begin exactly at ya
         constexpr int e = (kQ - (2 * R) % kQ) % kQ;
@@ -151,40 +264,86 @@ __global__ void __launch_bounds__(kMaxPairs * kItemsPerPair, 1) fbf_fused_kernel
         const int a0 = ya - R - e;
         const int steps = s0 + (len + kQ - 1) / kQ;
 
-        for (int s = 0; s < steps; ++s) {
-            const int a = a0 + s * kQ;
-            const int slot_base = (s * kQ) % RING;
-            __syncthreads();  // previous step's combine is done with colout/fring
+        __syncthreads();  // previous segment completely done with fstage / colmap
+        for (int xl = tid; xl < GW; xl += nthreads) colmap[xl] = map_border(x0 - R + xl, p.width, p.border);
+        __syncthreads();
 
-            // ---- gen: channel pairs of the Q new input rows -------------------
+        // Stage the f tile of step `st` into fstage[st & 1]; returns whether TMA was used.
+        auto stage_f = [&](int st) -> bool {
+            float* fs = fstage + (st & 1) * kQ * FSW;
+            const int a = a0 + st * kQ;
+            const int lo = max(a, ya - R), hi = min(a + kQ, yb + R);
+            if (cols_interior && lo >= 0 && hi <= p.height && lo < hi) {
+                if (tid < 32) {  // warp 0: one bulk copy per needed row
+                    if (tid == 0) {
+                        fence_proxy_async();
+                        mbar_arrive_expect_tx(&mbar[st & 1], (unsigned)(sizeof(float) * FSW * (hi - lo)));
+                    }
+                    __syncwarp();
+                    const int gy = lo + tid;
+                    if (gy < hi)
+                        tma_bulk_g2s(fs + (gy - a) * FSW, src + (long long)(gy - p.src_row0) * p.src_pitch + xs,
+                                     (unsigned)(sizeof(float) * FSW), &mbar[st & 1]);
+                }
+                return true;
+            }
             for (int pix = tid; pix < kQ * GW; pix += nthreads) {
                 const int q = pix / GW, xl = pix - q * GW;
-                const int gy = a + q, gx = x0 - R + xl;
-                const bool need = gy >= ya - R && gy < yb + R;
-                const int my = need ? map_border(gy, p.height, p.border) : -1;
-                const int mx = map_border(gx, p.width, p.border);
-                const bool valid = my >= 0 && mx >= 0;
-                const float f = valid ? __ldg(src + (long long)(my - p.src_row0) * p.src_pitch + mx) : 0.f;
-                if (xl >= R && xl < R + kTW) fring[((slot_base + q) % RING) * kTW + (xl - R)] = f;
-                float2* g = gen + q * GS + xl;
-                int pi = 0;
-                for (int kk = 0; kk < p.n_k; ++kk) {
-                    if (p.k_lo + kk == 0) {
-                        g[(size_t)pi * kQ * GS] = valid ? make_float2(f, 1.f) : make_float2(0.f, 0.f);
-                        pi += 1;
-                    } else {
-                        float2 cs = harmonic(f, p.kinv[kk]);
+                const int gy = a + q;
+                const int my = (gy >= lo && gy < hi) ? map_border(gy, p.height, p.border) : -1;
+                const int mx = colmap[xl];
+                float* d = fs + q * FSW + xoff + xl;
+                if (my >= 0 && mx >= 0)
+                    cp_async4(d, src + (long long)(my - p.src_row0) * p.src_pitch + mx);
+                else
+                    *d = 0.f;
+            }
+            cp_async_commit();
+            return false;
+        };
+        bool tma_next = stage_f(0);
+
+        for (int s = 0; s < steps; ++s) {
+            const int a = a0 + s * kQ;
+            const int blk = s % RB;
+            if (tma_next) {
+                if (s & 1) { mbar_wait(&mbar[1], phase1); phase1 ^= 1u; }
+                else       { mbar_wait(&mbar[0], phase0); phase0 ^= 1u; }
+            }
+            cp_async_wait_all();
+            __syncthreads();  // fstage[s&1] landed; previous combine done with colout/fring
+            tma_next = (s + 1 < steps) ? stage_f(s + 1) : false;
+
+            // ---- gen: channel pairs of the Q new input rows -------------------
+            {
+                const float* fs = fstage + (s & 1) * kQ * FSW;
+                const int lo = max(a, ya - R), hi = min(a + kQ, yb + R);
+                for (int pix = tid; pix < kQ * GW; pix += nthreads) {
+                    const int q = pix / GW, xl = pix - q * GW;
+                    const int gy = a + q;
+                    const bool valid = gy >= lo && gy < hi && colmap[xl] >= 0 && (p.border != 2 || (gy >= 0 && gy < p.height));
+                    const float f = valid ? fs[q * FSW + xoff + xl] : 0.f;
+                    if (xl >= R && xl < R + kTW) fring[(blk * kQ + q) * kTW + (xl - R)] = f;
+                    float2* g = gen + q * GS + xl;
+                    if (zk) g[0] = valid ? make_float2(f, 1.f) : make_float2(0.f, 0.f);
+                    if (NKR > 0) {
+                        const float2 c1 = harmonic(f, p.kinv1);
+                        float2 cs = (p.k_lo <= 1) ? c1 : harmonic(f, p.kinv_first);
                         if (!valid) cs = make_float2(0.f, 0.f);
-                        g[(size_t)pi * kQ * GS] = make_float2(cs.x * f, cs.y * f);
-                        g[(size_t)(pi + 1) * kQ * GS] = cs;
-                        pi += 2;
+                        float2* gk = g + (size_t)zk * kQ * GS;
+#pragma unroll
+                        for (int kk = 0; kk < NKR; ++kk) {
+                            gk[(size_t)(2 * kk) * kQ * GS] = make_float2(cs.x * f, cs.y * f);
+                            gk[(size_t)(2 * kk + 1) * kQ * GS] = cs;
+                            if (kk + 1 < NKR) cs = rotate(cs, c1);
+                        }
                     }
                 }
             }
             __syncthreads();
 
-            // ---- row pass: horizontal taps, ring[pair][slot][x] ----------------
-            {  // blockDim.x == n_items: one item per thread
+            // ---- row pass: horizontal taps into ring block blk -----------------
+            {  // blockDim.x == np * kItemsPerPair: one item per thread
                 const int q = tid % kQ;
                 const int xc = (tid / kQ) % (kTW / kP);
                 const int pr = tid / (kQ * (kTW / kP));
@@ -206,7 +365,7 @@ __global__ void __launch_bounds__(kMaxPairs * kItemsPerPair, 1) fbf_fused_kernel
                         }
                     }
                 }
-                float4* hout = reinterpret_cast<float4*>(ring + ((size_t)pr * RING + (slot_base + q) % RING) * RS + xc * kP);
+                float4* hout = reinterpret_cast<float4*>(ring + ((size_t)pr * RROWS + blk * kQ + q) * RS + xc * kP);
 #pragma unroll
                 for (int o = 0; o < kP / 2; ++o)
                     hout[o] = make_float4(accp[2 * o].x, accp[2 * o].y, accp[2 * o + 1].x, accp[2 * o + 1].y);
@@ -218,26 +377,8 @@ __global__ void __launch_bounds__(kMaxPairs * kItemsPerPair, 1) fbf_fused_kernel
             // (gen was last read by the row pass, so colout may overwrite it)
             {
                 const int x = tid % kTW;
-                const int g = (tid / kTW) % (kQ / kP);
-                const int pr = tid / (kTW * (kQ / kP));
-                const int q0 = g * kP;
-                const float2* rp = ring + (size_t)pr * RING * RS + x;
-                int sl = (slot_base + kQ + q0) % RING;
-                float2 accp[kP];
-#pragma unroll
-                for (int o = 0; o < kP; ++o) accp[o] = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int i = 0; i < kP + 2 * R; ++i) {
-                    const float2 v = rp[sl * RS];
-                    sl = (sl + 1 == RING) ? 0 : sl + 1;
-#pragma unroll
-                    for (int o = 0; o < kP; ++o) {
-                        const int d = i - o;
-                        if (d >= 0 && d <= 2 * R) accp[o] = ffma2(v, p.taps[d >= R ? d - R : R - d], accp[o]);
-                    }
-                }
-#pragma unroll
-                for (int o = 0; o < kP; ++o) colout[((size_t)pr * kQ + q0 + o) * kTW + x] = accp[o];
+                const int pr = tid / kTW;
+                column_pass<R>(ring + (size_t)pr * RROWS * RS, blk, x, p.taps, colout + (size_t)pr * kQ * kTW + x);
             }
             __syncthreads();
 
@@ -246,7 +387,10 @@ __global__ void __launch_bounds__(kMaxPairs * kItemsPerPair, 1) fbf_fused_kernel
                 const int q = pix / kTW, x = pix - q * kTW;
                 const int y = a - R + q, gxo = x0 + x;
                 if (y >= yb || gxo >= p.width) continue;
-                const float f = fring[((slot_base + kQ + R + q) % RING) * kTW + x];
+                int fr = blk * kQ + q - R;
+                fr += fr < 0 ? RROWS : 0;
+                fr += fr < 0 ? RROWS : 0;
+                const float f = fring[fr * kTW + x];
                 float num = 0.f, den = 0.f;
                 const long long ai = (long long)(y - p.out_row0) * p.width + gxo;
                 if (!p.first_chunk) {
@@ -254,21 +398,24 @@ __global__ void __launch_bounds__(kMaxPairs * kItemsPerPair, 1) fbf_fused_kernel
                     num = nd.x;
                     den = nd.y;
                 }
-                int pi = 0;
-                for (int kk = 0; kk < p.n_k; ++kk) {
-                    const float ck = p.coeff[kk];
-                    if (p.k_lo + kk == 0) {
-                        const float2 g0 = colout[((size_t)pi * kQ + q) * kTW + x];
-                        num += ck * g0.x;
-                        den += ck * g0.y;
-                        pi += 1;
-                    } else {
-                        const float2 cs = harmonic(f, p.kinv[kk]);
-                        const float2 gn = colout[((size_t)pi * kQ + q) * kTW + x];
-                        const float2 gd = colout[((size_t)(pi + 1) * kQ + q) * kTW + x];
+                const float2* go = colout + q * kTW + x;
+                if (zk) {
+                    const float2 g0 = go[0];
+                    num += p.coeff[0] * g0.x;
+                    den += p.coeff[0] * g0.y;
+                }
+                if (NKR > 0) {
+                    const float2 c1 = harmonic(f, p.kinv1);
+                    float2 cs = (p.k_lo <= 1) ? c1 : harmonic(f, p.kinv_first);
+                    const float2* gk = go + (size_t)zk * kQ * kTW;
+#pragma unroll
+                    for (int kk = 0; kk < NKR; ++kk) {
+                        const float ck = p.coeff[zk + kk];
+                        const float2 gn = gk[(size_t)(2 * kk) * kQ * kTW];
+                        const float2 gd = gk[(size_t)(2 * kk + 1) * kQ * kTW];
                         num += ck * (cs.x * gn.x + cs.y * gn.y);
                         den += ck * (cs.x * gd.x + cs.y * gd.y);
-                        pi += 2;
+                        if (kk + 1 < NKR) cs = rotate(cs, c1);
                     }
                 }
                 if (p.last_chunk) {
@@ -286,18 +433,18 @@ __global__ void __launch_bounds__(kMaxPairs * kItemsPerPair, 1) fbf_fused_kernel
     if (tid == 0 && p.fallbacks && *s_fallbacks) atomicAdd(p.fallbacks, (unsigned long long)*s_fallbacks);
 }
 
-template <int R>
+template <int R, int NKR>
 cudaError_t launch_fused(const Params& p, int grid, cudaStream_t stream) {
     using G = Geometry<R>;
     const size_t smem = G::smem_bytes(p.n_pairs);
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fbf_fused_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(fbf_fused_kernel<R, NKR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)kSmemLimit);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    fbf_fused_kernel<R><<<grid, p.n_pairs * kItemsPerPair, smem, stream>>>(p);
+    fbf_fused_kernel<R, NKR><<<grid, p.n_pairs * kItemsPerPair, smem, stream>>>(p);
     return cudaGetLastError();
 }
 
