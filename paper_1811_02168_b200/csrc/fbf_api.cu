@@ -32,7 +32,8 @@ namespace fbf_dev {
 #define FBF_EXTERN1(R, N) \
     extern template cudaError_t launch_fused<R, N>(const Params&, int, cudaStream_t);
 #define FBF_EXTERN(R) \
-    FBF_EXTERN1(R, 0) FBF_EXTERN1(R, 1) FBF_EXTERN1(R, 2) FBF_EXTERN1(R, 3) FBF_EXTERN1(R, 4) FBF_EXTERN1(R, 5)
+    FBF_EXTERN1(R, 0) FBF_EXTERN1(R, 1) FBF_EXTERN1(R, 2) FBF_EXTERN1(R, 3) FBF_EXTERN1(R, 4) FBF_EXTERN1(R, 5) \
+    FBF_EXTERN1(R, 6) FBF_EXTERN1(R, 7)
 FBF_EXTERN(1) FBF_EXTERN(2) FBF_EXTERN(3) FBF_EXTERN(4) FBF_EXTERN(5) FBF_EXTERN(6) FBF_EXTERN(7)
 FBF_EXTERN(8) FBF_EXTERN(9) FBF_EXTERN(10) FBF_EXTERN(11) FBF_EXTERN(12) FBF_EXTERN(13)
 FBF_EXTERN(14) FBF_EXTERN(15) FBF_EXTERN(16) FBF_EXTERN(17) FBF_EXTERN(18) FBF_EXTERN(19)
@@ -56,7 +57,7 @@ template <int R>
 RadiusEntry entry() {
     using G = Geometry<R>;
     return {{&launch_fused<R, 0>, &launch_fused<R, 1>, &launch_fused<R, 2>, &launch_fused<R, 3>,
-             &launch_fused<R, 4>, &launch_fused<R, 5>},
+             &launch_fused<R, 4>, &launch_fused<R, 5>, &launch_fused<R, 6>, &launch_fused<R, 7>},
             {0, G::max_pairs(1), G::max_pairs(2)},
             G::FSW,
             G::pair_bytes,
@@ -293,8 +294,8 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
         p.first_chunk = ci == 0;
         p.last_chunk = ci + 1 == plan.chunks.size();
         for (int kk = 0; kk < c.n_k; ++kk) p.coeff[kk] = (float)a.c[c.k_lo + kk];
-        p.kinv1 = 1.0 / (2.0 * a.T + 1.0);
-        p.kinv_first = (double)std::max(c.k_lo, 1) / (2.0 * a.T + 1.0);
+        p.inv_period = (float)(1.0 / (2.0 * a.T + 1.0));
+        p.k_first = std::max(c.k_lo, 1);
         const cudaError_t e = ent.launch[nkr](p, grid, stream);
         if (e != cudaSuccess) return cuda_fail(e, "fbf_fused_kernel launch");
         g_launches.fetch_add(1, std::memory_order_relaxed);
