@@ -277,9 +277,16 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
     for (int j = 0; j <= r; ++j)
         p.taps[j] = (float)std::exp(-((double)j * j) / (2.0 * theta * theta));
     // interior row spans go through the TMA bulk-copy engine when rows are 16-byte aligned
-    static const bool no_tma = std::getenv("FBF_NO_TMA") != nullptr;
-    p.use_tma = !no_tma && job.width % 4 == 0 && ((uintptr_t)job.d_src & 15) == 0 &&
-                (job.n_frames == 1 || job.src_frame_stride % 4 == 0);
+    // Interior f rows: element cp.async by default (measured fastest on B200:
+    // profiles/r01_stage_modes.txt); FBF_STAGE=bulk routes them through the TMA
+    // bulk-copy engine (needs 16-byte aligned rows).
+    static const int stage_mode = [] {
+        const char* e = std::getenv("FBF_STAGE");
+        return e && std::strcmp(e, "bulk") == 0 ? 1 : 0;
+    }();
+    const bool aligned = job.width % 4 == 0 && ((uintptr_t)job.d_src & 15) == 0 &&
+                         (job.n_frames == 1 || job.src_frame_stride % 4 == 0);
+    p.use_tma = aligned ? stage_mode : 0;
     // persistent grid: CTAs per SM x SMs, but keep segments at least a few steps long
     const long long min_seg = 4 * fbf_dev::kQ;
     const long long want = (p.total_units + min_seg - 1) / min_seg;

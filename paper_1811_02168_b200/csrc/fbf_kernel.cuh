@@ -18,11 +18,10 @@
 //   * A segment is streamed in steps of Q=8 input rows. Producer warps run
 //     stage + gen + row for step s while consumer warps run col + comb for
 //     step s-1; ring blocks are handed over with full/empty mbarriers.
-//       stage: the f tile of the NEXT step (Q rows x (TW+2r) columns) is
-//              fetched asynchronously: one TMA bulk copy per row
-//              (cp.async.bulk, mbarrier complete_tx) for interior tiles,
-//              border-mapped per-pixel cp.async at the image edges (the copy
-//              engine cannot mirror).
+//       stage: a loader warp fetches f tiles (Q rows x (TW+2r) columns) up to
+//              three steps ahead: one TMA bulk copy per row (cp.async.bulk,
+//              mbarrier complete_tx) for interior tiles, border-mapped
+//              element loads at the image edges (the copy engine cannot mirror).
 //       gen  : channel pairs (f, 1) for k = 0 and (C_k f, S_k f), (C_k, S_k)
 //              for k >= 1, with C_k + i S_k = exp(i k nu f) from one
 //              double-reduced MUFU sincos and the angle-addition recurrence.
@@ -47,18 +46,39 @@
 namespace fbf_dev {
 
 constexpr int kTW = 32;          // output columns per strip
-constexpr int kQ = 8;            // input rows per pipeline step
+#ifndef FBF_Q
+#define FBF_Q 8
+#endif
+constexpr int kQ = FBF_Q;        // input rows per pipeline step
 constexpr int kP = 8;            // outputs per thread item (row and column passes)
 constexpr int kMaxKR = 7;        // k >= 1 terms per launch (template parameter NKR <= kMaxKR)
 constexpr int kMaxPairs = 1 + 2 * kMaxKR;
 constexpr int kMaxRadius = 32;
 constexpr int kItemsPerPair = kQ * kTW / kP;  // 32 threads (one warp) per channel pair and role
-constexpr int kMaxThreads = 2 * kMaxPairs * kItemsPerPair;
+constexpr int kMaxThreads = 2 * kMaxPairs * kItemsPerPair + 32;
 constexpr size_t kSmemLimit = 232448;          // 227 KB opt-in per block on sm_100
 constexpr size_t kSmemPerSM = 233472;          // 228 KB per SM
 constexpr size_t kSmemReservedPerBlock = 1024;
 
-static_assert(kQ == kP, "one column-pass row group per step");
+static_assert(kQ % kP == 0, "column-pass row groups tile the step");
+
+#ifdef FBF_PHASES
+// dev instrumentation: per-role cycle counters (thread 0 of each role)
+__device__ unsigned long long g_phase_cycles[16];
+__device__ unsigned long long g_cta_cycles[1024];
+#define FBF_PHASE_T0() long long _ph_t = clock64()
+#define FBF_PHASE(i)                                                        \
+    do {                                                                    \
+        if (tid == 0) {                                                     \
+            long long _n = clock64();                                       \
+            atomicAdd(&g_phase_cycles[i], (unsigned long long)(_n - _ph_t)); \
+            _ph_t = _n;                                                     \
+        }                                                                   \
+    } while (0)
+#else
+#define FBF_PHASE_T0()
+#define FBF_PHASE(i)
+#endif
 
 struct Params {
     const float* src;            // frame 0, global row src_row0, column 0
@@ -77,7 +97,7 @@ struct Params {
     int k_first;                 // first k >= 1 of the chunk
     int first_chunk, last_chunk;
     int n_strips;
-    int use_tma;
+    int use_tma;                 // interior f tiles through the TMA bulk-copy engine
     long long total_units;       // n_frames * n_strips * out_rows
     float taps[kMaxRadius + 1];  // taps[j] = exp(-j^2 / (2 theta^2)), j = |d|
     float coeff[kMaxKR + 1];     // c_k of the chunk, ascending k
@@ -93,14 +113,14 @@ struct Geometry {
     static constexpr int RBX = RB + 1;                           // + the block being produced
     static constexpr int RROWS = RBX * kQ;                       // ring rows
     static constexpr int RS = kTW + 2;                           // ring stride (float2), RS/2 odd
-    static constexpr size_t fstage_bytes = sizeof(float) * 2 * kQ * FSW;  // multiple of 128
-    static constexpr size_t bar_bytes = 8 * (2 + 2 * RBX) + 8;            // mbarriers + counter
+    static constexpr int NFS = 3;                                // f staging buffers (loader runs ahead)
+    static constexpr size_t fstage_bytes = sizeof(float) * NFS * kQ * FSW;  // multiple of 128
+    static constexpr size_t bar_bytes = 8 * (2 * NFS + 2 * RBX) + 8;        // mbarriers + counter
     static constexpr size_t misc_bytes = (bar_bytes + 127) / 128 * 128;
-    static constexpr size_t colmap_bytes = sizeof(int) * ((GW + 3) / 4 * 4);
     static constexpr size_t fring_bytes = sizeof(float) * RROWS * kTW;
-    static constexpr size_t fixed_bytes = fstage_bytes + misc_bytes + colmap_bytes + fring_bytes;
+    static constexpr size_t fixed_bytes = fstage_bytes + misc_bytes + fring_bytes;
     static constexpr size_t pair_bytes = sizeof(float2) * (size_t)(kQ * GS + kQ * kTW + RROWS * RS);
-    static size_t smem_bytes(int pairs) { return fixed_bytes + pair_bytes * pairs; }
+    static constexpr size_t smem_bytes(int pairs) { return fixed_bytes + pair_bytes * pairs; }
     static int max_pairs(int blocks_per_sm) {
         size_t budget = kSmemPerSM / blocks_per_sm - kSmemReservedPerBlock;
         if (budget > kSmemLimit) budget = kSmemLimit;
@@ -138,6 +158,33 @@ __device__ __forceinline__ float2 rotate(float2 cs, float2 c1) {
     return make_float2(fmaf(cs.x, c1.x, -(cs.y * c1.y)), fmaf(cs.y, c1.x, cs.x * c1.y));
 }
 
+// Packed forms for two adjacent pixels: (C, S) hold the two pixels' cosines and
+// sines, per-lane arithmetic identical to rotate() / harmonic1().
+struct CS2 {
+    float2 c, s;
+};
+__device__ __forceinline__ CS2 harmonic1x2(float2 f, float inv_period) {
+    float2 t = __fmul2_rn(f, make_float2(inv_period, inv_period));
+    t = make_float2(t.x - rintf(t.x), t.y - rintf(t.y));
+    t = __fmul2_rn(t, make_float2(6.28318530717958647692f, 6.28318530717958647692f));
+    CS2 r;
+    __sincosf(t.x, &r.s.x, &r.c.x);
+    __sincosf(t.y, &r.s.y, &r.c.y);
+    return r;
+}
+__device__ __forceinline__ CS2 rotate2(CS2 v, CS2 w, float2 nws) {  // nws = -w.s
+    CS2 r;
+    r.c = __ffma2_rn(v.c, w.c, __fmul2_rn(v.s, nws));
+    r.s = __ffma2_rn(v.s, w.c, __fmul2_rn(v.c, w.s));
+    return r;
+}
+__device__ __forceinline__ CS2 harmonic_first2(CS2 c1, int k_first) {
+    const float2 nws = make_float2(-c1.s.x, -c1.s.y);
+    CS2 cs = c1;
+    for (int k = 1; k < k_first; ++k) cs = rotate2(cs, c1, nws);
+    return cs;
+}
+
 __device__ __forceinline__ float2 harmonic_first(float2 c1, int k_first) {
     float2 cs = c1;
     for (int k = 1; k < k_first; ++k) cs = rotate(cs, c1);
@@ -158,6 +205,14 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 __device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc));
 }
+__device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc));
+}
+// arrive-on of `bar` triggered when this thread's prior cp.async copies land
+// (the pending count is incremented now and decremented on completion)
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -168,6 +223,11 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// raise the expected transaction bytes of the current phase (no arrival)
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
@@ -193,10 +253,10 @@ __device__ __forceinline__ void tma_bulk_g2s(float* smem_dst, const float* gsrc,
                  : "memory");
 }
 
-// Vertical pass for the kQ output rows of global step g. The window rows
-// j in [-2R, kP) (relative to block g) resolve to (block, row) at compile
-// time, so every load is a fixed offset from one of RB block pointers.
-template <int R>
+// Vertical pass for output rows [Q0, Q0 + kP) of global step g. The window
+// rows j in [Q0 - 2R, Q0 + kP) (relative to block g) resolve to (block, row)
+// at compile time, so every load is a fixed offset from one of RB block pointers.
+template <int R, int Q0>
 __device__ __forceinline__ void column_pass(const float2* __restrict__ ring_pair, int blk, int x,
                                             const float* taps, float2* out_col) {
     using G = Geometry<R>;
@@ -213,7 +273,7 @@ __device__ __forceinline__ void column_pass(const float2* __restrict__ ring_pair
     for (int o = 0; o < kP; ++o) acc[o] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int i = 0; i < kP + 2 * R; ++i) {
-        const int j = i - 2 * R;                          // compile-time
+        const int j = Q0 + i - 2 * R;                     // compile-time
         const int b = j >= 0 ? 0 : (-j + kQ - 1) / kQ;    // blocks back
         const float2 v = bptr[b][(j + b * kQ) * RS];
 #pragma unroll
@@ -223,35 +283,53 @@ __device__ __forceinline__ void column_pass(const float2* __restrict__ ring_pair
         }
     }
 #pragma unroll
-    for (int o = 0; o < kP; ++o) out_col[o * kTW] = acc[o];
+    for (int o = 0; o < kP; ++o) {  // planar: [q][component][TW]
+        float* oc = reinterpret_cast<float*>(out_col) + (Q0 + o) * 2 * kTW;
+        oc[0] = acc[o].x;
+        oc[kTW] = acc[o].y;
+    }
 }
 
+// Two CTAs per SM when a full chunk (1 + 2 NKR pairs) fits in half the shared
+// memory: their warp roles interleave. The register budget follows.
 template <int R, int NKR>
-__global__ void __launch_bounds__(2 * (1 + 2 * NKR) * kItemsPerPair, 1) fbf_fused_kernel(const __grid_constant__ Params p) {
+constexpr int blocks_per_sm() {
+    return Geometry<R>::smem_bytes(1 + 2 * NKR) + kSmemReservedPerBlock <= kSmemPerSM / 2 ? 2 : 1;
+}
+
+// Warp roles: [0, np) warps = producer (gen + row pass), [np, 2np) = consumer
+// (column pass + combine), last warp = loader (f tiles via the TMA bulk-copy
+// engine or border-mapped loads, up to NFS steps ahead).
+template <int R, int NKR>
+__global__ void __launch_bounds__(2 * (1 + 2 * NKR) * kItemsPerPair + 32, (blocks_per_sm<R, NKR>()))
+    fbf_fused_kernel(const __grid_constant__ Params p) {
     using G = Geometry<R>;
     constexpr int GW = G::GW, GS = G::GS, FSW = G::FSW, RB = G::RB, RBX = G::RBX, RROWS = G::RROWS, RS = G::RS;
+    constexpr int NFS = G::NFS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int np = p.n_pairs;
-    float* fstage = reinterpret_cast<float*>(smem_raw);                         // [2][Q][FSW]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + G::fstage_bytes);   // fs[2], full[RBX], empty[RBX]
-    uint64_t* fs_bar = bars;
-    uint64_t* full_bar = bars + 2;
-    uint64_t* empty_bar = bars + 2 + RBX;
-    unsigned int* s_fallbacks = reinterpret_cast<unsigned int*>(bars + 2 + 2 * RBX);
-    int* colmap = reinterpret_cast<int*>(smem_raw + G::fstage_bytes + G::misc_bytes);  // [GW]
-    float* fring = reinterpret_cast<float*>(smem_raw + G::fstage_bytes + G::misc_bytes + G::colmap_bytes);
+    float* fstage = reinterpret_cast<float*>(smem_raw);                         // [NFS][Q][FSW]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + G::fstage_bytes);
+    uint64_t* fs_full = bars;                    // [NFS] loader -> producer
+    uint64_t* fs_empty = bars + NFS;             // [NFS] producer -> loader
+    uint64_t* full_bar = bars + 2 * NFS;         // [RBX] producer -> consumer
+    uint64_t* empty_bar = bars + 2 * NFS + RBX;  // [RBX] consumer -> producer
+    unsigned int* s_fallbacks = reinterpret_cast<unsigned int*>(bars + 2 * NFS + 2 * RBX);
+    float* fring = reinterpret_cast<float*>(smem_raw + G::fstage_bytes + G::misc_bytes);  // [RROWS][TW]
     float2* gen = reinterpret_cast<float2*>(fring + RROWS * kTW);  // [np][Q][GS]     (producer)
     float2* colout = gen + (size_t)np * kQ * GS;                   // [np][Q][TW]     (consumer)
     float2* ring = colout + (size_t)np * kQ * kTW;                 // [np][RROWS][RS] (handoff)
 
-    const int nrole = np * kItemsPerPair;  // threads per role
-    const bool producer = threadIdx.x < nrole;
-    const int tid = producer ? threadIdx.x : threadIdx.x - nrole;
+    const int nrole = np * kItemsPerPair;  // threads per compute role
+    const int role = threadIdx.x < nrole ? 0 : (threadIdx.x < 2 * nrole ? 1 : 2);
+    const int tid = threadIdx.x - role * nrole;
     const int zk = p.k_lo == 0 ? 1 : 0;  // k = 0 contributes the single pair (f, 1)
     if (threadIdx.x == 0) {
         *s_fallbacks = 0u;
-        mbar_init(&fs_bar[0], 1);
-        mbar_init(&fs_bar[1], 1);
+        for (int b = 0; b < NFS; ++b) {
+            mbar_init(&fs_full[b], 1);
+            mbar_init(&fs_empty[b], 1);
+        }
         for (int b = 0; b < RBX; ++b) {
             mbar_init(&full_bar[b], 1);
             mbar_init(&empty_bar[b], 1);
@@ -259,14 +337,18 @@ __global__ void __launch_bounds__(2 * (1 + 2 * NKR) * kItemsPerPair, 1) fbf_fuse
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    unsigned fs_phase0 = 0, fs_phase1 = 0;
+#ifdef FBF_PHASES
+    const long long _cta_t0 = clock64();
+    unsigned long long _gt0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_gt0));
+#endif
 
     // this CTA's contiguous share of the (frame, strip, row) units
     const long long U = p.total_units;
     const long long u_begin = U * blockIdx.x / gridDim.x;
     const long long u_end = U * (blockIdx.x + 1) / gridDim.x;
     const long long per_frame = (long long)p.n_strips * p.out_rows;
-    int gstep = 0;  // global step counter: ring block = step % RBX
+    int gstep = 0;  // global step counter: ring block = gstep % RBX, f buffer = gstep % NFS
 
     for (long long u = u_begin; u < u_end;) {
         const int frame = (int)(u / per_frame);
@@ -284,93 +366,143 @@ __global__ void __launch_bounds__(2 * (1 + 2 * NKR) * kItemsPerPair, 1) fbf_fuse
         const int a0 = ya - R - e;
         const int steps = s0 + (len + kQ - 1) / kQ;
 
-        if (producer) {
-            // =========================== PRODUCER ===========================
+        if (role == 2) {
+            // ============================ LOADER ============================
+            // fstage row q holds f at columns [xs, xs + FSW), xs = (x0 - R) rounded down
+            // to 16 bytes. Each needed row is fetched as ONE TMA bulk copy of its in-image
+            // span plus, at the image edges, 4-byte cp.async of the border-mapped columns
+            // (the copy engine cannot mirror). Rows/columns outside the image under the
+            // zero border are never read: gen treats them as zero.
             const float* src = p.src + (long long)frame * p.src_frame_stride;
-            // interior strips copy 16-byte-aligned row spans [xs, xs + FSW) with the copy engine
-            const int xs = (x0 - R) & ~3, xoff = (x0 - R) - xs;
-            const bool cols_interior = p.use_tma && xs >= 0 && xs + FSW <= p.width;
-            named_sync(1, nrole);  // previous segment done with fstage / colmap
-            for (int xl = tid; xl < GW; xl += nrole) colmap[xl] = map_border(x0 - R + xl, p.width, p.border);
-            named_sync(1, nrole);
-
-            // Stage the f tile of step `st` into fstage[st & 1]; returns whether TMA was used.
-            auto stage_f = [&](int st) -> bool {
-                float* fs = fstage + (st & 1) * kQ * FSW;
-                const int a = a0 + st * kQ;
-                const int lo = max(a, ya - R), hi = min(a + kQ, yb + R);
-                if (cols_interior && lo >= 0 && hi <= p.height && lo < hi) {
-                    if (tid < 32) {  // warp 0: one bulk copy per needed row
-                        if (tid == 0) {
-                            fence_proxy_async();
-                            mbar_arrive_expect_tx(&fs_bar[st & 1], (unsigned)(sizeof(float) * FSW * (hi - lo)));
-                        }
-                        __syncwarp();
-                        const int gy = lo + tid;
-                        if (gy < hi)
-                            tma_bulk_g2s(fs + (gy - a) * FSW, src + (long long)(gy - p.src_row0) * p.src_pitch + xs,
-                                         (unsigned)(sizeof(float) * FSW), &fs_bar[st & 1]);
-                    }
-                    return true;
+            const int xs = (x0 - R) & ~3;
+            const int c0 = max(xs, 0), c1 = min(xs + FSW, p.width);  // in-image span
+            const bool bulk = p.use_tma && c1 > c0;
+            // this lane's share of the element-copied columns: the border-mapped
+            // ones at the image edges (bulk) or the whole window (no bulk)
+            constexpr int LCOLS = (GW + 31) / 32;
+            int lmx[LCOLS], loff[LCOLS];
+            {
+                const int wlo = x0 - R, whi = x0 + kTW + R;
+                const int blo = bulk ? c0 : whi, bhi = bulk ? c1 : whi;  // bulk-covered span
+                const int nleft = max(0, min(blo, whi) - wlo), nright = max(0, whi - max(bhi, wlo));
+                const int ncols = bulk ? nleft + nright : GW;
+#pragma unroll
+                for (int j = 0; j < LCOLS; ++j) {
+                    const int c = tid + 32 * j;
+                    const int gx = bulk ? (c < nleft ? wlo + c : max(bhi, wlo) + (c - nleft)) : wlo + c;
+                    lmx[j] = c < ncols ? map_border(gx, p.width, p.border) : -1;
+                    loff[j] = gx - xs;
                 }
-                for (int pix = tid; pix < kQ * GW; pix += nrole) {
-                    const int q = pix / GW, xl = pix - q * GW;
+            }
+            for (int s = 0; s < steps; ++s) {
+                const int g = gstep + s;
+                const int fb = g % NFS;
+                if (g >= NFS) mbar_wait(&fs_empty[fb], (unsigned)((g / NFS - 1) & 1));
+                float* fs = fstage + fb * kQ * FSW;
+                const int a = a0 + s * kQ;
+                const int lo = max(a, ya - R), hi = min(a + kQ, yb + R);
+                int nrows_src = 0;  // needed rows that read the image
+                for (int gy = lo; gy < hi; ++gy) nrows_src += map_border(gy, p.height, p.border) >= 0;
+                if (bulk && p.use_tma == 1 && tid == 0 && nrows_src > 0)
+                    mbar_expect_tx(&fs_full[fb], (unsigned)(sizeof(float) * (c1 - c0) * nrows_src));
+                __syncwarp();
+                if (bulk && p.use_tma == 2 && c0 + 4 * tid < c1) {
+                    // 16-byte cp.async: lane = 16-byte column chunk of the in-image span
+#pragma unroll
+                    for (int q = 0; q < kQ; ++q) {
+                        const int gy = a + q;
+                        const int my = (gy >= lo && gy < hi) ? map_border(gy, p.height, p.border) : -1;
+                        if (my >= 0)
+                            cp_async16(fs + q * FSW + (c0 - xs) + 4 * tid,
+                                       src + (long long)(my - p.src_row0) * p.src_pitch + c0 + 4 * tid);
+                    }
+                }
+                if (bulk && p.use_tma == 1 && tid < kQ) {
+                    const int gy = a + tid;
+                    const int my = (gy >= lo && gy < hi) ? map_border(gy, p.height, p.border) : -1;
+                    if (my >= 0)
+                        tma_bulk_g2s(fs + tid * FSW + (c0 - xs), src + (long long)(my - p.src_row0) * p.src_pitch + c0,
+                                     (unsigned)(sizeof(float) * (c1 - c0)), &fs_full[fb]);
+                }
+                // columns of the window the bulk copy did not cover (precomputed per segment)
+#pragma unroll
+                for (int q = 0; q < kQ; ++q) {
                     const int gy = a + q;
                     const int my = (gy >= lo && gy < hi) ? map_border(gy, p.height, p.border) : -1;
-                    const int mx = colmap[xl];
-                    float* d = fs + q * FSW + xoff + xl;
-                    if (my >= 0 && mx >= 0)
-                        cp_async4(d, src + (long long)(my - p.src_row0) * p.src_pitch + mx);
-                    else
-                        *d = 0.f;
+                    if (my < 0) continue;
+                    const float* srow = src + (long long)(my - p.src_row0) * p.src_pitch;
+#pragma unroll
+                    for (int j = 0; j < LCOLS; ++j)
+                        if (lmx[j] >= 0) cp_async4(fs + q * FSW + loff[j], srow + lmx[j]);
                 }
-                cp_async_commit();
-                return false;
-            };
-            bool tma_next = stage_f(0);
-
+                cp_async_mbar_arrive(&fs_full[fb]);
+                __syncwarp();
+                if (tid == 0) mbar_arrive(&fs_full[fb]);
+            }
+        } else if (role == 0) {
+            // =========================== PRODUCER ===========================
+            const int xoff = (x0 - R) - ((x0 - R) & ~3);
+            FBF_PHASE_T0();
             for (int s = 0; s < steps; ++s) {
                 const int g = gstep + s;
                 const int blk = g % RBX;
+                const int fb = g % NFS;
                 const int a = a0 + s * kQ;
-                if (tma_next) {
-                    if (s & 1) { mbar_wait(&fs_bar[1], fs_phase1); fs_phase1 ^= 1u; }
-                    else       { mbar_wait(&fs_bar[0], fs_phase0); fs_phase0 ^= 1u; }
-                }
-                cp_async_wait_all();
-                named_sync(1, nrole);  // fstage[s&1] complete; gen buffer free (row pass s-1 done)
-                tma_next = (s + 1 < steps) ? stage_f(s + 1) : false;
+                FBF_PHASE(0);
+                mbar_wait(&fs_full[fb], (unsigned)((g / NFS) & 1));
+                FBF_PHASE(1);
                 // ring/fring block `blk` is free once the consumer finished step g - 2
                 if (g >= RBX) mbar_wait(&empty_bar[blk], (unsigned)((g / RBX - 1) & 1));
+                FBF_PHASE(3);
 
                 // ---- gen: channel pairs of the Q new input rows ----------------
+                // one item = two adjacent pixels (xl, xl + 1): packed FP32 math and
+                // 16-byte stores of both pixels' (channel, channel) pairs
                 {
-                    const float* fs = fstage + (s & 1) * kQ * FSW;
+                    const float* fs = fstage + fb * kQ * FSW;
                     const int lo = max(a, ya - R), hi = min(a + kQ, yb + R);
-                    for (int pix = tid; pix < kQ * GW; pix += nrole) {
-                        const int q = pix / GW, xl = pix - q * GW;
-                        const int gy = a + q;
-                        const bool valid = gy >= lo && gy < hi && colmap[xl] >= 0 &&
-                                           (p.border != 2 || (gy >= 0 && gy < p.height));
-                        const float f = valid ? fs[q * FSW + xoff + xl] : 0.f;
-                        if (xl >= R && xl < R + kTW) fring[(blk * kQ + q) * kTW + (xl - R)] = f;
-                        float2* gp = gen + q * GS + xl;
-                        if (zk) gp[0] = valid ? make_float2(f, 1.f) : make_float2(0.f, 0.f);
-                        if (NKR > 0) {
-                            const float2 c1 = harmonic1(f, p.inv_period);
-                            float2 cs = harmonic_first(c1, p.k_first);
-                            if (!valid) cs = make_float2(0.f, 0.f);
-                            float2* gk = gp + (size_t)zk * kQ * GS;
+                    constexpr int HGW = GW / 2;  // GW = TW + 2R is even
+                    constexpr int GITER = NKR > 0 ? (kQ * HGW + 2 * NKR * kItemsPerPair - 1) / (2 * NKR * kItemsPerPair) : 1;
+                    for (int base = 0; base < kQ * HGW; base += GITER * nrole) {
 #pragma unroll
-                            for (int kk = 0; kk < NKR; ++kk) {
-                                gk[(size_t)(2 * kk) * kQ * GS] = make_float2(cs.x * f, cs.y * f);
-                                gk[(size_t)(2 * kk + 1) * kQ * GS] = cs;
-                                if (kk + 1 < NKR) cs = rotate(cs, c1);
+                        for (int it = 0; it < GITER; ++it) {
+                            const int item = base + it * nrole + tid;
+                            if (item < kQ * HGW) {
+                                const int q = item / HGW, xl = 2 * (item - q * HGW);
+                                const int gy = a + q, gx = x0 - R + xl;
+                                const bool rowok = gy >= lo && gy < hi && (p.border != 2 || (gy >= 0 && gy < p.height));
+                                const bool va = rowok && (p.border != 2 || (gx >= 0 && gx < p.width));
+                                const bool vb = rowok && (p.border != 2 || (gx + 1 >= 0 && gx + 1 < p.width));
+                                const float* fp = fs + q * FSW + xoff + xl;
+                                const float2 f = make_float2(va ? fp[0] : 0.f, vb ? fp[1] : 0.f);
+                                float* fr = fring + (blk * kQ + q) * kTW + (xl - R);
+                                if (xl >= R && xl < R + kTW) fr[0] = f.x;
+                                if (xl + 1 >= R && xl + 1 < R + kTW) fr[1] = f.y;
+                                float4* gp = reinterpret_cast<float4*>(gen + q * GS + xl);
+                                if (zk) gp[0] = make_float4(f.x, va ? 1.f : 0.f, f.y, vb ? 1.f : 0.f);
+                                if (NKR > 0) {
+                                    const CS2 c1 = harmonic1x2(f, p.inv_period);
+                                    const float2 nws = make_float2(-c1.s.x, -c1.s.y);
+                                    CS2 cs = harmonic_first2(c1, p.k_first);
+                                    if (!va) cs.c.x = cs.s.x = 0.f;
+                                    if (!vb) cs.c.y = cs.s.y = 0.f;
+                                    float4* gk = gp + (size_t)zk * kQ * GS / 2;
+#pragma unroll
+                                    for (int kk = 0; kk < NKR; ++kk) {
+                                        const float2 cf = __fmul2_rn(cs.c, f), sf = __fmul2_rn(cs.s, f);
+                                        gk[(size_t)(2 * kk) * kQ * GS / 2] = make_float4(cf.x, sf.x, cf.y, sf.y);
+                                        gk[(size_t)(2 * kk + 1) * kQ * GS / 2] = make_float4(cs.c.x, cs.s.x, cs.c.y, cs.s.y);
+                                        if (kk + 1 < NKR) cs = rotate2(cs, c1, nws);
+                                    }
+                                }
                             }
                         }
                     }
                 }
-                named_sync(1, nrole);
+                FBF_PHASE(4);
+                named_sync(1, nrole);  // gen complete (and fstage[fb] fully read)
+                if (tid == 0) mbar_arrive(&fs_empty[fb]);
+                FBF_PHASE(5);
 
                 // ---- row pass: horizontal taps into ring block blk -------------
                 {  // nrole == np * kItemsPerPair: one item per producer thread
@@ -402,74 +534,109 @@ __global__ void __launch_bounds__(2 * (1 + 2 * NKR) * kItemsPerPair, 1) fbf_fuse
                     for (int o = 0; o < kP / 2; ++o)
                         hout[o] = make_float4(accp[2 * o].x, accp[2 * o].y, accp[2 * o + 1].x, accp[2 * o + 1].y);
                 }
-                named_sync(1, nrole);                   // every row of block blk written
+                FBF_PHASE(6);
+                named_sync(1, nrole);                       // every row of block blk written; gen free
                 if (tid == 0) mbar_arrive(&full_bar[blk]);  // release to the consumer
+                FBF_PHASE(7);
             }
         } else {
             // =========================== CONSUMER ===========================
             float* dst = p.dst + (long long)frame * p.dst_frame_stride;
             float2* acc = p.acc ? p.acc + (long long)frame * p.acc_frame_stride : nullptr;
+            FBF_PHASE_T0();
             for (int s = 0; s < steps; ++s) {
                 const int g = gstep + s;
                 const int blk = g % RBX;
                 const int a = a0 + s * kQ;
+                FBF_PHASE(8);
                 mbar_wait(&full_bar[blk], (unsigned)((g / RBX) & 1));
+                FBF_PHASE(9);
                 if (s >= s0) {  // warm-up steps only fill the ring
                     // ---- column pass: vertical taps over the ring -> colout ----
                     {
                         const int x = tid % kTW;
-                        const int pr = tid / kTW;
-                        column_pass<R>(ring + (size_t)pr * RROWS * RS, blk, x, p.taps,
-                                       colout + (size_t)pr * kQ * kTW + x);
+                        const int grp = (tid / kTW) % (kQ / kP);  // warp-uniform row group
+                        const int pr = tid / (kTW * (kQ / kP));
+                        const float2* rp = ring + (size_t)pr * RROWS * RS;
+                        float2* oc = reinterpret_cast<float2*>(reinterpret_cast<float*>(colout) +
+                                                               (size_t)pr * kQ * 2 * kTW + x);
+                        if (kQ / kP == 1 || grp == 0)
+                            column_pass<R, 0>(rp, blk, x, p.taps, oc);
+                        else
+                            column_pass<R, (kQ / kP > 1 ? kP : 0)>(rp, blk, x, p.taps, oc);
                     }
+                    FBF_PHASE(10);
                     named_sync(2, nrole);
+                    FBF_PHASE(11);
 
                     // ---- combine -----------------------------------------------
-                    for (int pix = tid; pix < kQ * kTW; pix += nrole) {
-                        const int q = pix / kTW, x = pix - q * kTW;
+                    // one item = two adjacent output pixels, packed FP32 math
+                    constexpr int HTW = kTW / 2;
+                    constexpr int CITER = NKR > 0 ? (kQ * HTW + 2 * NKR * kItemsPerPair - 1) / (2 * NKR * kItemsPerPair) : 4;
+#pragma unroll
+                    for (int it = 0; it < CITER; ++it) {
+                        const int item = it * nrole + tid;
+                        const int q = item / HTW, x = 2 * (item - q * HTW);
                         const int y = a - R + q, gxo = x0 + x;
-                        if (y >= yb || gxo >= p.width) continue;
-                        int fr = blk * kQ + q - R;
-                        while (fr < 0) fr += RROWS;
-                        const float f = fring[fr * kTW + x];
-                        float num = 0.f, den = 0.f;
+                        if (item >= kQ * HTW || y >= yb || gxo >= p.width) continue;
+                        const bool vb = gxo + 1 < p.width;
+                        int frow = blk * kQ + q - R;
+                        while (frow < 0) frow += RROWS;
+                        const float2 f = *reinterpret_cast<const float2*>(fring + frow * kTW + x);
+                        float2 num = make_float2(0.f, 0.f), den = make_float2(0.f, 0.f);
                         const long long ai = (long long)(y - p.out_row0) * p.width + gxo;
                         if (!p.first_chunk) {
-                            const float2 nd = acc[ai];
-                            num = nd.x;
-                            den = nd.y;
+                            const float2 nda = acc[ai], ndb = vb ? acc[ai + 1] : make_float2(0.f, 0.f);
+                            num = make_float2(nda.x, ndb.x);
+                            den = make_float2(nda.y, ndb.y);
                         }
-                        const float2* go = colout + q * kTW + x;
+                        // planar colout: [pair][q][component][TW]
+                        const float* go = reinterpret_cast<const float*>(colout) + q * 2 * kTW + x;
+                        constexpr int PSTR = kQ * 2 * kTW;  // floats per pair
                         if (zk) {
-                            const float2 g0 = go[0];
-                            num += p.coeff[0] * g0.x;
-                            den += p.coeff[0] * g0.y;
+                            const float2 gx0 = *reinterpret_cast<const float2*>(go);
+                            const float2 gy0 = *reinterpret_cast<const float2*>(go + kTW);
+                            const float2 c0 = make_float2(p.coeff[0], p.coeff[0]);
+                            num = __ffma2_rn(c0, gx0, num);
+                            den = __ffma2_rn(c0, gy0, den);
                         }
                         if (NKR > 0) {
-                            const float2 c1 = harmonic1(f, p.inv_period);
-                            float2 cs = harmonic_first(c1, p.k_first);
-                            const float2* gk = go + (size_t)zk * kQ * kTW;
+                            const CS2 c1 = harmonic1x2(f, p.inv_period);
+                            const float2 nws = make_float2(-c1.s.x, -c1.s.y);
+                            CS2 cs = harmonic_first2(c1, p.k_first);
+                            const float* gk = go + zk * PSTR;
 #pragma unroll
                             for (int kk = 0; kk < NKR; ++kk) {
-                                const float ck = p.coeff[zk + kk];
-                                const float2 gn = gk[(size_t)(2 * kk) * kQ * kTW];
-                                const float2 gd = gk[(size_t)(2 * kk + 1) * kQ * kTW];
-                                num += ck * (cs.x * gn.x + cs.y * gn.y);
-                                den += ck * (cs.x * gd.x + cs.y * gd.y);
-                                if (kk + 1 < NKR) cs = rotate(cs, c1);
+                                const float2 ck = make_float2(p.coeff[zk + kk], p.coeff[zk + kk]);
+                                const float* gn = gk + (2 * kk) * PSTR;
+                                const float* gd = gk + (2 * kk + 1) * PSTR;
+                                const float2 gnx = *reinterpret_cast<const float2*>(gn);
+                                const float2 gny = *reinterpret_cast<const float2*>(gn + kTW);
+                                const float2 gdx = *reinterpret_cast<const float2*>(gd);
+                                const float2 gdy = *reinterpret_cast<const float2*>(gd + kTW);
+                                num = __ffma2_rn(ck, __ffma2_rn(cs.s, gny, __fmul2_rn(cs.c, gnx)), num);
+                                den = __ffma2_rn(ck, __ffma2_rn(cs.s, gdy, __fmul2_rn(cs.c, gdx)), den);
+                                if (kk + 1 < NKR) cs = rotate2(cs, c1, nws);
                             }
                         }
+                        float* drow = dst + (long long)(y - p.out_row0) * p.dst_pitch + gxo;
                         if (p.last_chunk) {
-                            float o = f;
-                            if (den > 1e-12f) o = num / den;
-                            else atomicAdd(s_fallbacks, 1u);
-                            dst[(long long)(y - p.out_row0) * p.dst_pitch + gxo] = o;
+                            float oa = f.x, ob = f.y;
+                            unsigned nfb = 0;
+                            if (den.x > 1e-12f) oa = __fdividef(num.x, den.x); else ++nfb;
+                            if (den.y > 1e-12f) ob = __fdividef(num.y, den.y); else nfb += vb;
+                            if (nfb) atomicAdd(s_fallbacks, nfb);
+                            drow[0] = oa;
+                            if (vb) drow[1] = ob;
                         } else {
-                            acc[ai] = make_float2(num, den);
+                            acc[ai] = make_float2(num.x, den.x);
+                            if (vb) acc[ai + 1] = make_float2(num.y, den.y);
                         }
                     }
                 }
+                FBF_PHASE(12);
                 named_sync(2, nrole);  // all consumer reads of the ring / colout done
+                FBF_PHASE(13);
                 // the oldest block of this step's window is no longer needed
                 if (tid == 0 && g - RB + 1 >= 0) mbar_arrive(&empty_bar[(g - RB + 1) % RBX]);
             }
@@ -477,6 +644,15 @@ __global__ void __launch_bounds__(2 * (1 + 2 * NKR) * kItemsPerPair, 1) fbf_fuse
         gstep += steps;
     }
     __syncthreads();
+#ifdef FBF_PHASES
+    if (threadIdx.x == 0) {
+        unsigned long long _gt1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_gt1));
+        atomicMax(&g_phase_cycles[14], (unsigned long long)(clock64() - _cta_t0));
+        if (blockIdx.x < 1024) g_cta_cycles[blockIdx.x] = (unsigned long long)(clock64() - _cta_t0);
+        atomicAdd(&g_phase_cycles[15], (unsigned long long)(clock64() - _cta_t0) * 1000ull / (_gt1 - _gt0 + 1));
+    }
+#endif
     if (threadIdx.x == 0 && p.fallbacks && *s_fallbacks) atomicAdd(p.fallbacks, (unsigned long long)*s_fallbacks);
 }
 
@@ -491,7 +667,7 @@ cudaError_t launch_fused(const Params& p, int grid, cudaStream_t stream) {
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    fbf_fused_kernel<R, NKR><<<grid, 2 * p.n_pairs * kItemsPerPair, smem, stream>>>(p);
+    fbf_fused_kernel<R, NKR><<<grid, 2 * p.n_pairs * kItemsPerPair + 32, smem, stream>>>(p);
     return cudaGetLastError();
 }
 
