@@ -231,9 +231,10 @@ def test_shapes_radii_and_chunking(gpu, oracle, shape, theta, sigma, eps):
 
 @pytest.mark.parametrize("name", ["c0", "c1", "c2", "c3", "c4"])
 def test_baseline_configs(gpu, oracle, name):
-    # P13: every BASELINE config -- (K, T) as the reference chooses them, GPU within 1e-2
-    # of the oracle. Small configs are compared in full; the large ones on a crop (same
-    # parameters, the crop treated as the image) plus full-size properties.
+    # P13: every BASELINE config at its full size -- (K, T) as the reference chooses them,
+    # GPU within 1e-2 of the oracle: c0 in full, c3 on three frames, c1/c2/c4 on
+    # top/middle/bottom row bands of the full-image result (exact semantics), plus
+    # shard invariance.
     from paper_1811_02168_b200 import configs
     fb = gpu
     cfg = configs.CONFIGS[name]
@@ -256,16 +257,26 @@ def test_baseline_configs(gpu, oracle, name):
             assert np.abs(got - ref).max() <= TOL
             assert np.array_equal(out[f], fb.fast_bilateral(frames[f], k, a))
         return
-    full = configs.make_frame(cfg) if name != "c4" else None
-    if name == "c4":  # 16384^2 is built on the fly at reduced height for memory/time
-        full = fb.field_image(cfg.width, 2048, cfg.sites, cfg.noise, cfg.seed)
-    crop = np.ascontiguousarray(full[:256, :384])
-    got, fbk = gpu_filter(fb, crop, cfg.theta, a)
-    ref, _ = oracle_filter(oracle, crop, cfg.theta, a)
-    assert fbk == 0 and np.abs(got - ref).max() <= TOL
-    # full-size properties: values within the input range, bands == single device
+    full = configs.make_frame(cfg)
     out = fb.fast_bilateral(full, k, a)
-    assert out.min() >= full.min() - TOL and out.max() <= full.max() + TOL
+    r = cfg.radius
+    # exact semantics at full size on row bands: rows [y0, y0 + n) of the full-image
+    # result equal the oracle run on the halo-extended band (the border mapping only
+    # reaches rows inside it), for a top, a middle and a bottom band
+    H = full.shape[0]
+    for y0 in (0, H // 2 + 3, H - 16):
+        s0, s1 = max(0, y0 - r), min(H, y0 + 16 + r)
+        sub = full[s0:s1]
+        if s0 > 0 and s1 < H:
+            ref, _ = oracle_filter(oracle, sub, cfg.theta, a)
+            got = out[y0:y0 + 16]
+            assert np.abs(got - ref[y0 - s0:y0 - s0 + 16]).max() <= TOL
+        elif s0 == 0:
+            ref, _ = oracle_filter(oracle, sub, cfg.theta, a)
+            assert np.abs(out[0:16] - ref[0:16]).max() <= TOL
+        else:
+            ref, _ = oracle_filter(oracle, sub, cfg.theta, a)
+            assert np.abs(out[H - 16:H] - ref[-16:]).max() <= TOL
     assert np.array_equal(fb.fast_bilateral_bands(full, k, a, n_gpus=1), out)
 
 
