@@ -32,8 +32,7 @@ namespace fbf_dev {
 #define FBF_EXTERN1(R, N) \
     extern template cudaError_t launch_fused<R, N>(const Params&, int, cudaStream_t);
 #define FBF_EXTERN(R) \
-    FBF_EXTERN1(R, 0) FBF_EXTERN1(R, 1) FBF_EXTERN1(R, 2) FBF_EXTERN1(R, 3) FBF_EXTERN1(R, 4) FBF_EXTERN1(R, 5) \
-    FBF_EXTERN1(R, 6) FBF_EXTERN1(R, 7)
+    FBF_EXTERN1(R, 0) FBF_EXTERN1(R, 1) FBF_EXTERN1(R, 2) FBF_EXTERN1(R, 3) FBF_EXTERN1(R, 4)
 FBF_EXTERN(1) FBF_EXTERN(2) FBF_EXTERN(3) FBF_EXTERN(4) FBF_EXTERN(5) FBF_EXTERN(6) FBF_EXTERN(7)
 FBF_EXTERN(8) FBF_EXTERN(9) FBF_EXTERN(10) FBF_EXTERN(11) FBF_EXTERN(12) FBF_EXTERN(13)
 FBF_EXTERN(14) FBF_EXTERN(15) FBF_EXTERN(16) FBF_EXTERN(17) FBF_EXTERN(18) FBF_EXTERN(19)
@@ -57,7 +56,7 @@ template <int R>
 RadiusEntry entry() {
     using G = Geometry<R>;
     return {{&launch_fused<R, 0>, &launch_fused<R, 1>, &launch_fused<R, 2>, &launch_fused<R, 3>,
-             &launch_fused<R, 4>, &launch_fused<R, 5>, &launch_fused<R, 6>, &launch_fused<R, 7>},
+             &launch_fused<R, 4>},
             {0, G::max_pairs(1), G::max_pairs(2)},
             G::FSW,
             G::pair_bytes,
@@ -217,21 +216,11 @@ std::vector<Chunk> split_chunks(int K, int max_pairs) {
     return out;
 }
 
-// Two CTAs per SM hide each other's barrier and generation phases; use them
-// unless that needs more coefficient chunks (each chunk re-streams the image).
-// FBF_BLOCKS_PER_SM=1|2 overrides (tuning).
+// One CTA per SM (the three warp roles already overlap latency-bound and
+// FFMA2-bound phases; registers allow no second CTA).
 Plan make_plan(int K, int r) {
     const auto& ent = fbf_dev::radius_entry(r);
-    Plan p1{split_chunks(K, ent.max_pairs[1]), 1};
-    Plan p2{split_chunks(K, ent.max_pairs[2]), 2};
-    static const int forced = [] {
-        const char* e = std::getenv("FBF_BLOCKS_PER_SM");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (forced == 1) return p1;
-    if (forced == 2 && ent.max_pairs[2] >= 2) return p2;
-    if (ent.max_pairs[2] >= 2 && p2.chunks.size() <= p1.chunks.size()) return p2;
-    return p1;
+    return Plan{split_chunks(K, ent.max_pairs[1]), 1};
 }
 
 struct Job {

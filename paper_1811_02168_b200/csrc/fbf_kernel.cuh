@@ -51,11 +51,14 @@ constexpr int kTW = 32;          // output columns per strip
 #endif
 constexpr int kQ = FBF_Q;        // input rows per pipeline step
 constexpr int kP = 8;            // outputs per thread item (row and column passes)
-constexpr int kMaxKR = 7;        // k >= 1 terms per launch (template parameter NKR <= kMaxKR)
+constexpr int kMaxKR = 4;        // k >= 1 terms per launch (template parameter NKR <= kMaxKR)
 constexpr int kMaxPairs = 1 + 2 * kMaxKR;
 constexpr int kMaxRadius = 32;
 constexpr int kItemsPerPair = kQ * kTW / kP;  // 32 threads (one warp) per channel pair and role
-constexpr int kMaxThreads = 2 * kMaxPairs * kItemsPerPair + 32;
+constexpr int kRoles = 2;        // pair warps and gen warps scale with the pairs
+constexpr int kCombThreads = kQ * kTW / 2;  // combine warps: one pixel pair per thread
+constexpr int kExtraThreads = kCombThreads + 32;  // + combine + loader
+constexpr int kMaxThreads = kRoles * kMaxPairs * kItemsPerPair + kExtraThreads;
 constexpr size_t kSmemLimit = 232448;          // 227 KB opt-in per block on sm_100
 constexpr size_t kSmemPerSM = 233472;          // 228 KB per SM
 constexpr size_t kSmemReservedPerBlock = 1024;
@@ -110,16 +113,16 @@ struct Geometry {
     static constexpr int GS = GW + ((2 - GW % 4) + 4) % 4;       // gen stride (float2), GS/2 odd
     static constexpr int FSW = (GW + 3 + 3) / 4 * 4;             // f staging row: GW + 16B-alignment slack
     static constexpr int RB = 1 + (2 * R + kQ - 1) / kQ;         // ring blocks a column pass reads
-    static constexpr int RBX = RB + 1;                           // + the block being produced
-    static constexpr int RROWS = RBX * kQ;                       // ring rows
+    static constexpr int RROWS = RB * kQ;                        // ring rows (private to a pair warp)
     static constexpr int RS = kTW + 2;                           // ring stride (float2), RS/2 odd
     static constexpr int NFS = 3;                                // f staging buffers (loader runs ahead)
+    static constexpr int NGB = 2;                                // gen buffers (gen runs ahead)
+    static constexpr int NCB = 2;                                // column-result buffers
     static constexpr size_t fstage_bytes = sizeof(float) * NFS * kQ * FSW;  // multiple of 128
-    static constexpr size_t bar_bytes = 8 * (2 * NFS + 2 * RBX) + 8;        // mbarriers + counter
+    static constexpr size_t bar_bytes = 8 * (2 * NFS + 2 * NGB + 2 * NCB) + 8;  // mbarriers + counter
     static constexpr size_t misc_bytes = (bar_bytes + 127) / 128 * 128;
-    static constexpr size_t fring_bytes = sizeof(float) * RROWS * kTW;
-    static constexpr size_t fixed_bytes = fstage_bytes + misc_bytes + fring_bytes;
-    static constexpr size_t pair_bytes = sizeof(float2) * (size_t)(kQ * GS + kQ * kTW + RROWS * RS);
+    static constexpr size_t fixed_bytes = fstage_bytes + misc_bytes;
+    static constexpr size_t pair_bytes = sizeof(float2) * (size_t)(NGB * kQ * GS + NCB * kQ * kTW + RROWS * RS);
     static constexpr size_t smem_bytes(int pairs) { return fixed_bytes + pair_bytes * pairs; }
     static int max_pairs(int blocks_per_sm) {
         size_t budget = kSmemPerSM / blocks_per_sm - kSmemReservedPerBlock;
@@ -156,6 +159,24 @@ __device__ __forceinline__ float2 harmonic1(float f, float inv_period) {
 // depend on how k is split into chunks.
 __device__ __forceinline__ float2 rotate(float2 cs, float2 c1) {
     return make_float2(fmaf(cs.x, c1.x, -(cs.y * c1.y)), fmaf(cs.y, c1.x, cs.x * c1.y));
+}
+
+// Complex rotation z * w with packed FP32: t = z.x (w.x, w.y); z' = z.y (-w.y, w.x) + t,
+// u = (-w.y, w.x) precomputed. gen and combine share this exact sequence.
+__device__ __forceinline__ float2 cmul_rot(float2 z, float2 w, float2 u) {
+    return __ffma2_rn(make_float2(z.y, z.y), u, __fmul2_rn(make_float2(z.x, z.x), w));
+}
+__device__ __forceinline__ float2 harmonic1c(float f, float inv_period) {
+    float t = f * inv_period;
+    t -= rintf(t);
+    float sn, cs;
+    __sincosf(t * 6.28318530717958647692f, &sn, &cs);
+    return make_float2(cs, sn);
+}
+__device__ __forceinline__ float2 harmonic_firstc(float2 w, float2 u, int k_first) {
+    float2 z = w;
+    for (int k = 1; k < k_first; ++k) z = cmul_rot(z, w, u);
+    return z;
 }
 
 // Packed forms for two adjacent pixels: (C, S) hold the two pixels' cosines and
@@ -230,15 +251,18 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
     asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+// Blocking wait for the phase with the given parity. The suspend-time hint lets
+// the hardware park the warp until the phase completes instead of spinning
+// (a spinning try_wait loop costs issue slots the FFMA2 warps need).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
         "@!P1 bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(1000000u)
         : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() {
@@ -258,14 +282,14 @@ __device__ __forceinline__ void tma_bulk_g2s(float* smem_dst, const float* gsrc,
 // at compile time, so every load is a fixed offset from one of RB block pointers.
 template <int R, int Q0>
 __device__ __forceinline__ void column_pass(const float2* __restrict__ ring_pair, int blk, int x,
-                                            const float* taps, float2* out_col) {
+                                            const float* taps, float* out_col) {
     using G = Geometry<R>;
-    constexpr int RB = G::RB, RBX = G::RBX, RS = G::RS;
+    constexpr int RB = G::RB, RS = G::RS;
     const float2* bptr[RB];
 #pragma unroll
-    for (int b = 0; b < RB; ++b) {  // bptr[b] = block (blk - b) mod RBX
+    for (int b = 0; b < RB; ++b) {  // bptr[b] = block (blk - b) mod RB
         int bb = blk - b;
-        bb += bb < 0 ? RBX : 0;
+        bb += bb < 0 ? RB : 0;
         bptr[b] = ring_pair + bb * kQ * RS + x;
     }
     float2 acc[kP];
@@ -284,56 +308,70 @@ __device__ __forceinline__ void column_pass(const float2* __restrict__ ring_pair
     }
 #pragma unroll
     for (int o = 0; o < kP; ++o) {  // planar: [q][component][TW]
-        float* oc = reinterpret_cast<float*>(out_col) + (Q0 + o) * 2 * kTW;
+        float* oc = out_col + (Q0 + o) * 2 * kTW;
         oc[0] = acc[o].x;
         oc[kTW] = acc[o].y;
     }
 }
 
-// Two CTAs per SM when a full chunk (1 + 2 NKR pairs) fits in half the shared
-// memory: their warp roles interleave. The register budget follows.
-template <int R, int NKR>
-constexpr int blocks_per_sm() {
-    return Geometry<R>::smem_bytes(1 + 2 * NKR) + kSmemReservedPerBlock <= kSmemPerSM / 2 ? 2 : 1;
-}
+// Warp roles (np = channel pairs of the launch):
+//   PAIR (np warps) : warp p owns channel pair p: horizontal pass of the step's
+//                     Q rows into ITS OWN ring, then the vertical pass of the step
+//                     from that ring into a column buffer -- no cross-warp handoff
+//                     between the two passes
+//   GEN  (np warps) : channel pairs of the next step into one of 2 gen buffers
+//   COMB (4 warps)  : combine + divide, one output pixel pair per thread
+//   LOAD (1 warp)   : f tiles into one of 3 staging buffers
+// Handoffs GEN -> PAIR -> COMB and LOAD -> GEN are full/empty mbarrier pairs
+// with per-warp arrivals, so no role waits for a sibling warp.
 
-// Warp roles: [0, np) warps = producer (gen + row pass), [np, 2np) = consumer
-// (column pass + combine), last warp = loader (f tiles via the TMA bulk-copy
-// engine or border-mapped loads, up to NFS steps ahead).
+// Per-segment geometry shared by every role.
+struct Segment {
+    int frame, x0, ya, yb, a0, steps;
+};
+
 template <int R, int NKR>
-__global__ void __launch_bounds__(2 * (1 + 2 * NKR) * kItemsPerPair + 32, (blocks_per_sm<R, NKR>()))
+__global__ void __launch_bounds__(kRoles * (1 + 2 * NKR) * kItemsPerPair + kExtraThreads, 1)
     fbf_fused_kernel(const __grid_constant__ Params p) {
     using G = Geometry<R>;
-    constexpr int GW = G::GW, GS = G::GS, FSW = G::FSW, RB = G::RB, RBX = G::RBX, RROWS = G::RROWS, RS = G::RS;
-    constexpr int NFS = G::NFS;
+    constexpr int GW = G::GW, GS = G::GS, FSW = G::FSW, RB = G::RB, RROWS = G::RROWS, RS = G::RS;
+    constexpr int NFS = G::NFS, NGB = G::NGB, NCB = G::NCB;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int np = p.n_pairs;
     float* fstage = reinterpret_cast<float*>(smem_raw);                         // [NFS][Q][FSW]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + G::fstage_bytes);
-    uint64_t* fs_full = bars;                    // [NFS] loader -> producer
-    uint64_t* fs_empty = bars + NFS;             // [NFS] producer -> loader
-    uint64_t* full_bar = bars + 2 * NFS;         // [RBX] producer -> consumer
-    uint64_t* empty_bar = bars + 2 * NFS + RBX;  // [RBX] consumer -> producer
-    unsigned int* s_fallbacks = reinterpret_cast<unsigned int*>(bars + 2 * NFS + 2 * RBX);
-    float* fring = reinterpret_cast<float*>(smem_raw + G::fstage_bytes + G::misc_bytes);  // [RROWS][TW]
-    float2* gen = reinterpret_cast<float2*>(fring + RROWS * kTW);  // [np][Q][GS]     (producer)
-    float2* colout = gen + (size_t)np * kQ * GS;                   // [np][Q][TW]     (consumer)
-    float2* ring = colout + (size_t)np * kQ * kTW;                 // [np][RROWS][RS] (handoff)
+    uint64_t* fs_full = bars;                                // [NFS] LOAD -> GEN
+    uint64_t* fs_empty = fs_full + NFS;                      // [NFS] GEN  -> LOAD
+    uint64_t* gen_full = fs_empty + NFS;                     // [NGB] GEN  -> PAIR
+    uint64_t* gen_empty = gen_full + NGB;                    // [NGB] PAIR -> GEN
+    uint64_t* col_full = gen_empty + NGB;                    // [NCB] PAIR -> COMB
+    uint64_t* col_empty = col_full + NCB;                    // [NCB] COMB -> PAIR
+    unsigned int* s_fallbacks = reinterpret_cast<unsigned int*>(col_empty + NCB);
+    float2* gen = reinterpret_cast<float2*>(smem_raw + G::fstage_bytes + G::misc_bytes);  // [NGB][np][Q][GS]
+    float* colout = reinterpret_cast<float*>(gen + (size_t)NGB * np * kQ * GS);          // [NCB][np][Q][2][TW]
+    float2* ring = reinterpret_cast<float2*>(colout + (size_t)NCB * np * kQ * 2 * kTW);  // [np][RROWS][RS]
 
-    const int nrole = np * kItemsPerPair;  // threads per compute role
-    const int role = threadIdx.x < nrole ? 0 : (threadIdx.x < 2 * nrole ? 1 : 2);
-    const int tid = threadIdx.x - role * nrole;
+    const int nrole = np * kItemsPerPair;  // threads of the PAIR and GEN roles
+    // Warp slots: [PAIR | COMB | GEN | LOAD]; the scheduler favours higher warp ids,
+    // so the latency-bound chains (GEN, COMB) get first pick of the issue slots and the
+    // FFMA2 streams of the pair warps fill the rest.
+    int role, tid;  // role: 0 GEN, 1 PAIR, 3 LOAD, 4 COMB
+    {
+        const int t = threadIdx.x;
+        if (t < nrole)                          { role = 1; tid = t; }
+        else if (t < nrole + kCombThreads)      { role = 4; tid = t - nrole; }
+        else if (t < 2 * nrole + kCombThreads)  { role = 0; tid = t - nrole - kCombThreads; }
+        else                                    { role = 3; tid = t - 2 * nrole - kCombThreads; }
+    }
+    const int lane = threadIdx.x & 31;
     const int zk = p.k_lo == 0 ? 1 : 0;  // k = 0 contributes the single pair (f, 1)
     if (threadIdx.x == 0) {
         *s_fallbacks = 0u;
-        for (int b = 0; b < NFS; ++b) {
-            mbar_init(&fs_full[b], 1);
-            mbar_init(&fs_empty[b], 1);
-        }
-        for (int b = 0; b < RBX; ++b) {
-            mbar_init(&full_bar[b], 1);
-            mbar_init(&empty_bar[b], 1);
-        }
+        // every warp arrives on its own (no intra-role barrier): counts = warps
+        const unsigned nw = (unsigned)np, ncw = kCombThreads / 32;
+        for (int b = 0; b < NFS; ++b) { mbar_init(&fs_full[b], 1); mbar_init(&fs_empty[b], nw); }
+        for (int b = 0; b < NGB; ++b) { mbar_init(&gen_full[b], nw); mbar_init(&gen_empty[b], nw); }
+        for (int b = 0; b < NCB; ++b) { mbar_init(&col_full[b], nw); mbar_init(&col_empty[b], ncw); }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -348,37 +386,153 @@ __global__ void __launch_bounds__(2 * (1 + 2 * NKR) * kItemsPerPair + 32, (block
     const long long u_begin = U * blockIdx.x / gridDim.x;
     const long long u_end = U * (blockIdx.x + 1) / gridDim.x;
     const long long per_frame = (long long)p.n_strips * p.out_rows;
-    int gstep = 0;  // global step counter: ring block = gstep % RBX, f buffer = gstep % NFS
-
-    for (long long u = u_begin; u < u_end;) {
-        const int frame = (int)(u / per_frame);
+    // steps start e rows early so that output rows begin exactly at ya
+    constexpr int e = (kQ - (2 * R) % kQ) % kQ;
+    constexpr int s0 = (2 * R + e) / kQ;
+    auto segment_at = [&](long long u, long long& next) {
+        Segment sg;
+        sg.frame = (int)(u / per_frame);
         const long long rem = u % per_frame;
         const int strip = (int)(rem / p.out_rows);
         const int row = (int)(rem % p.out_rows);
         const int len = (int)min((long long)(p.out_rows - row), u_end - u);
-        u += len;
+        next = u + len;
+        sg.x0 = strip * kTW;
+        sg.ya = p.out_row0 + row;
+        sg.yb = sg.ya + len;
+        sg.a0 = sg.ya - R - e;
+        sg.steps = s0 + (len + kQ - 1) / kQ;
+        return sg;
+    };
 
-        const int x0 = strip * kTW;
-        const int ya = p.out_row0 + row, yb = ya + len;
-        // steps start e rows early so that output rows begin exactly at ya
-        constexpr int e = (kQ - (2 * R) % kQ) % kQ;
-        constexpr int s0 = (2 * R + e) / kQ;
-        const int a0 = ya - R - e;
-        const int steps = s0 + (len + kQ - 1) / kQ;
+    // ---- GEN: channel pairs of step s of segment sg into gen buffer gb --------------
+    // item = it * nrole + tid covers the two adjacent pixels (q, xl), (q, xl + 1).
+    constexpr int HGW = GW / 2;  // GW = TW + 2R is even
+    constexpr int GITER = NKR > 0 ? (kQ * HGW + 2 * NKR * kItemsPerPair - 1) / (2 * NKR * kItemsPerPair)
+                                  : (kQ * HGW + kItemsPerPair - 1) / kItemsPerPair;
+    auto gen_step = [&](const Segment& sg, int s, int fb, int gb) {
+        const int a = sg.a0 + s * kQ;
+        const int xoff = (sg.x0 - R) - ((sg.x0 - R) & ~3);
+        const float* fs = fstage + fb * kQ * FSW + xoff;
+        float2* gbuf = gen + (size_t)gb * np * kQ * GS;
+        const int lo = max(a, sg.ya - R), hi = min(a + kQ, sg.yb + R);
+        const bool zb = p.border == 2;
+        const float inv = p.inv_period;
+#pragma unroll
+        for (int it = 0; it < GITER; ++it) {
+            const int item = it * nrole + tid;
+            if (item < kQ * HGW) {
+                const int q = item / HGW, xl = 2 * (item - q * HGW);
+                const int gy = a + q, gx = sg.x0 - R + xl;
+                const bool rowok = gy >= lo && gy < hi && (!zb || (gy >= 0 && gy < p.height));
+                const bool va = rowok && (!zb || (gx >= 0 && gx < p.width));
+                const bool vb = rowok && (!zb || (gx + 1 >= 0 && gx + 1 < p.width));
+                const float2 f = make_float2(va ? fs[q * FSW + xl] : 0.f, vb ? fs[q * FSW + xl + 1] : 0.f);
+                float4* gp = reinterpret_cast<float4*>(gbuf + q * GS + xl);
+                if (zk) gp[0] = make_float4(f.x, va ? 1.f : 0.f, f.y, vb ? 1.f : 0.f);
+                if (NKR > 0) {
+                    const CS2 c1 = harmonic1x2(f, inv);
+                    const float2 nws = make_float2(-c1.s.x, -c1.s.y);
+                    CS2 cs = p.k_first > 1 ? harmonic_first2(c1, p.k_first) : c1;
+                    if (!va) cs.c.x = cs.s.x = 0.f;
+                    if (!vb) cs.c.y = cs.s.y = 0.f;
+                    float4* gk = gp + (size_t)zk * kQ * GS / 2;
+#pragma unroll
+                    for (int kk = 0; kk < NKR; ++kk) {
+                        const float2 cf = __fmul2_rn(cs.c, f), sf = __fmul2_rn(cs.s, f);
+                        gk[(size_t)(2 * kk) * kQ * GS / 2] = make_float4(cf.x, sf.x, cf.y, sf.y);
+                        gk[(size_t)(2 * kk + 1) * kQ * GS / 2] = make_float4(cs.c.x, cs.s.x, cs.c.y, cs.s.y);
+                        if (kk + 1 < NKR) cs = rotate2(cs, c1, nws);
+                    }
+                }
+            }
+        }
+    };
 
-        if (role == 2) {
-            // ============================ LOADER ============================
-            // fstage row q holds f at columns [xs, xs + FSW), xs = (x0 - R) rounded down
-            // to 16 bytes. Each needed row is fetched as ONE TMA bulk copy of its in-image
-            // span plus, at the image edges, 4-byte cp.async of the border-mapped columns
-            // (the copy engine cannot mirror). Rows/columns outside the image under the
-            // zero border are never read: gen treats them as zero.
-            const float* src = p.src + (long long)frame * p.src_frame_stride;
-            const int xs = (x0 - R) & ~3;
+    // ---- COMB: combine of step s of segment sg from column buffer cb -----------------
+    // one item = two adjacent output pixels per thread; f is re-read from the source
+    // image (L2-resident) so nothing but the column results travels through smem
+    auto combine_step = [&](const Segment& sg, int s, int cb) {
+        const int a = sg.a0 + s * kQ;
+        constexpr int HTW = kTW / 2;
+        static_assert(kCombThreads == kQ * HTW, "one combine item per thread");
+        const int q = tid / HTW, x = 2 * (tid - q * HTW);
+        const int y = a - R + q, gxo = sg.x0 + x;
+        if (y >= sg.yb || gxo >= p.width) return;
+        const bool vb = gxo + 1 < p.width;
+        const float* srow = p.src + (long long)sg.frame * p.src_frame_stride + (long long)(y - p.src_row0) * p.src_pitch;
+        const float2 f = make_float2(__ldg(srow + gxo), vb ? __ldg(srow + gxo + 1) : 0.f);
+        float* dst = p.dst + (long long)sg.frame * p.dst_frame_stride;
+        float2* acc = p.acc ? p.acc + (long long)sg.frame * p.acc_frame_stride : nullptr;
+        float2 num = make_float2(0.f, 0.f), den = make_float2(0.f, 0.f);
+        const long long ai = (long long)(y - p.out_row0) * p.width + gxo;
+        if (!p.first_chunk) {
+            const float2 nda = acc[ai], ndb = vb ? acc[ai + 1] : make_float2(0.f, 0.f);
+            num = make_float2(nda.x, ndb.x);
+            den = make_float2(nda.y, ndb.y);
+        }
+        // planar column results: [pair][q][component][TW]
+        const float* go = colout + (size_t)cb * np * kQ * 2 * kTW + q * 2 * kTW + x;
+        constexpr int PSTR = kQ * 2 * kTW;  // floats per pair
+        if (zk) {
+            const float2 gx0 = *reinterpret_cast<const float2*>(go);
+            const float2 gy0 = *reinterpret_cast<const float2*>(go + kTW);
+            const float2 c0 = make_float2(p.coeff[0], p.coeff[0]);
+            num = __ffma2_rn(c0, gx0, num);
+            den = __ffma2_rn(c0, gy0, den);
+        }
+        if (NKR > 0) {
+            const CS2 c1 = harmonic1x2(f, p.inv_period);
+            const float2 nws = make_float2(-c1.s.x, -c1.s.y);
+            CS2 cs = p.k_first > 1 ? harmonic_first2(c1, p.k_first) : c1;
+            const float* gk = go + zk * PSTR;
+#pragma unroll
+            for (int kk = 0; kk < NKR; ++kk) {
+                const float2 ck = make_float2(p.coeff[zk + kk], p.coeff[zk + kk]);
+                const float* gn = gk + (2 * kk) * PSTR;
+                const float* gd = gk + (2 * kk + 1) * PSTR;
+                const float2 gnx = *reinterpret_cast<const float2*>(gn);
+                const float2 gny = *reinterpret_cast<const float2*>(gn + kTW);
+                const float2 gdx = *reinterpret_cast<const float2*>(gd);
+                const float2 gdy = *reinterpret_cast<const float2*>(gd + kTW);
+                num = __ffma2_rn(ck, __ffma2_rn(cs.s, gny, __fmul2_rn(cs.c, gnx)), num);
+                den = __ffma2_rn(ck, __ffma2_rn(cs.s, gdy, __fmul2_rn(cs.c, gdx)), den);
+                if (kk + 1 < NKR) cs = rotate2(cs, c1, nws);
+            }
+        }
+        float* drow = dst + (long long)(y - p.out_row0) * p.dst_pitch + gxo;
+        if (p.last_chunk) {
+            float oa = f.x, ob = f.y;
+            unsigned nfb = 0;
+            if (den.x > 1e-12f) oa = __fdividef(num.x, den.x); else ++nfb;
+            if (den.y > 1e-12f) ob = __fdividef(num.y, den.y); else nfb += vb;
+            if (nfb) atomicAdd(s_fallbacks, nfb);
+            drow[0] = oa;
+            if (vb) drow[1] = ob;
+        } else {
+            acc[ai] = make_float2(num.x, den.x);
+            if (vb) acc[ai + 1] = make_float2(num.y, den.y);
+        }
+    };
+
+    int gstep = 0;  // global step counter: buffers are used round-robin over it
+    for (long long u = u_begin; u < u_end;) {
+        long long next;
+        const Segment sg = segment_at(u, next);
+        u = next;
+        const int steps = sg.steps;
+        const int x0 = sg.x0, ya = sg.ya, yb = sg.yb, a0 = sg.a0;
+        const int xs = (x0 - R) & ~3;  // f staging row origin (16-byte aligned)
+
+        if (role == 3) {
+            // ============================ LOAD ==============================
+            // fstage row q holds f at columns [xs, xs + FSW), border-mapped with
+            // 4-byte cp.async (or one TMA bulk copy per row for the in-image span,
+            // FBF_STAGE=bulk). Zero-border rows/columns outside the image are never
+            // read: GEN treats them as zero.
+            const float* src = p.src + (long long)sg.frame * p.src_frame_stride;
             const int c0 = max(xs, 0), c1 = min(xs + FSW, p.width);  // in-image span
             const bool bulk = p.use_tma && c1 > c0;
-            // this lane's share of the element-copied columns: the border-mapped
-            // ones at the image edges (bulk) or the whole window (no bulk)
             constexpr int LCOLS = (GW + 31) / 32;
             int lmx[LCOLS], loff[LCOLS];
             {
@@ -401,30 +555,25 @@ __global__ void __launch_bounds__(2 * (1 + 2 * NKR) * kItemsPerPair + 32, (block
                 float* fs = fstage + fb * kQ * FSW;
                 const int a = a0 + s * kQ;
                 const int lo = max(a, ya - R), hi = min(a + kQ, yb + R);
-                int nrows_src = 0;  // needed rows that read the image
-                for (int gy = lo; gy < hi; ++gy) nrows_src += map_border(gy, p.height, p.border) >= 0;
-                if (bulk && p.use_tma == 1 && tid == 0 && nrows_src > 0)
-                    mbar_expect_tx(&fs_full[fb], (unsigned)(sizeof(float) * (c1 - c0) * nrows_src));
-                __syncwarp();
-                if (bulk && p.use_tma == 2 && c0 + 4 * tid < c1) {
-                    // 16-byte cp.async: lane = 16-byte column chunk of the in-image span
-#pragma unroll
-                    for (int q = 0; q < kQ; ++q) {
-                        const int gy = a + q;
+#ifdef FBF_SKIP_LOAD
+                if (tid == 0) mbar_arrive(&fs_full[fb]);
+                continue;
+#endif
+                if (bulk) {
+                    int nrows_src = 0;  // needed rows that read the image
+                    for (int gy = lo; gy < hi; ++gy) nrows_src += map_border(gy, p.height, p.border) >= 0;
+                    if (tid == 0 && nrows_src > 0)
+                        mbar_expect_tx(&fs_full[fb], (unsigned)(sizeof(float) * (c1 - c0) * nrows_src));
+                    __syncwarp();
+                    if (tid < kQ) {
+                        const int gy = a + tid;
                         const int my = (gy >= lo && gy < hi) ? map_border(gy, p.height, p.border) : -1;
                         if (my >= 0)
-                            cp_async16(fs + q * FSW + (c0 - xs) + 4 * tid,
-                                       src + (long long)(my - p.src_row0) * p.src_pitch + c0 + 4 * tid);
+                            tma_bulk_g2s(fs + tid * FSW + (c0 - xs),
+                                         src + (long long)(my - p.src_row0) * p.src_pitch + c0,
+                                         (unsigned)(sizeof(float) * (c1 - c0)), &fs_full[fb]);
                     }
                 }
-                if (bulk && p.use_tma == 1 && tid < kQ) {
-                    const int gy = a + tid;
-                    const int my = (gy >= lo && gy < hi) ? map_border(gy, p.height, p.border) : -1;
-                    if (my >= 0)
-                        tma_bulk_g2s(fs + tid * FSW + (c0 - xs), src + (long long)(my - p.src_row0) * p.src_pitch + c0,
-                                     (unsigned)(sizeof(float) * (c1 - c0)), &fs_full[fb]);
-                }
-                // columns of the window the bulk copy did not cover (precomputed per segment)
 #pragma unroll
                 for (int q = 0; q < kQ; ++q) {
                     const int gy = a + q;
@@ -440,76 +589,58 @@ __global__ void __launch_bounds__(2 * (1 + 2 * NKR) * kItemsPerPair + 32, (block
                 if (tid == 0) mbar_arrive(&fs_full[fb]);
             }
         } else if (role == 0) {
-            // =========================== PRODUCER ===========================
-            const int xoff = (x0 - R) - ((x0 - R) & ~3);
+            // ============================= GEN ==============================
+            FBF_PHASE_T0();
+            for (int t = 0; t < steps; ++t) {
+                const int g = gstep + t;
+                const int fb = g % NFS, gb = g % NGB;
+                FBF_PHASE(0);
+                mbar_wait(&fs_full[fb], (unsigned)((g / NFS) & 1));
+                if (g >= NGB) mbar_wait(&gen_empty[gb], (unsigned)((g / NGB - 1) & 1));
+                FBF_PHASE(1);
+#ifndef FBF_SKIP_GEN
+                gen_step(sg, t, fb, gb);
+#endif
+                FBF_PHASE(4);
+                __syncwarp();  // this warp's part of gen buffer gb written, fstage fb read
+                if (lane == 0) {
+                    mbar_arrive(&fs_empty[fb]);
+                    mbar_arrive(&gen_full[gb]);
+                }
+                FBF_PHASE(5);
+            }
+        } else if (role == 4) {
+            // ============================ COMB ==============================
+            FBF_PHASE_T0();
+            for (int sc = 0; sc < steps; ++sc) {
+                const int g = gstep + sc;
+                const int cb = g % NCB;
+                mbar_wait(&col_full[cb], (unsigned)((g / NCB) & 1));
+                FBF_PHASE(12);
+#ifndef FBF_SKIP_COMB
+                if (sc >= s0) combine_step(sg, sc, cb);
+#endif
+                FBF_PHASE(13);
+                __syncwarp();  // this warp is done with column buffer cb
+                if (lane == 0) mbar_arrive(&col_empty[cb]);
+            }
+        } else {
+            // ============================= PAIR =============================
+            const int pr = tid / 32;  // this warp's channel pair
+            float2* myring = ring + (size_t)pr * RROWS * RS;
             FBF_PHASE_T0();
             for (int s = 0; s < steps; ++s) {
                 const int g = gstep + s;
-                const int blk = g % RBX;
-                const int fb = g % NFS;
-                const int a = a0 + s * kQ;
-                FBF_PHASE(0);
-                mbar_wait(&fs_full[fb], (unsigned)((g / NFS) & 1));
-                FBF_PHASE(1);
-                // ring/fring block `blk` is free once the consumer finished step g - 2
-                if (g >= RBX) mbar_wait(&empty_bar[blk], (unsigned)((g / RBX - 1) & 1));
+                const int gb = g % NGB, cb = g % NCB;
+                const int blk = g % RB;  // this step's ring block (this warp's private ring)
+                FBF_PHASE(2);
+                mbar_wait(&gen_full[gb], (unsigned)((g / NGB) & 1));
                 FBF_PHASE(3);
-
-                // ---- gen: channel pairs of the Q new input rows ----------------
-                // one item = two adjacent pixels (xl, xl + 1): packed FP32 math and
-                // 16-byte stores of both pixels' (channel, channel) pairs
-                {
-                    const float* fs = fstage + fb * kQ * FSW;
-                    const int lo = max(a, ya - R), hi = min(a + kQ, yb + R);
-                    constexpr int HGW = GW / 2;  // GW = TW + 2R is even
-                    constexpr int GITER = NKR > 0 ? (kQ * HGW + 2 * NKR * kItemsPerPair - 1) / (2 * NKR * kItemsPerPair) : 1;
-                    for (int base = 0; base < kQ * HGW; base += GITER * nrole) {
-#pragma unroll
-                        for (int it = 0; it < GITER; ++it) {
-                            const int item = base + it * nrole + tid;
-                            if (item < kQ * HGW) {
-                                const int q = item / HGW, xl = 2 * (item - q * HGW);
-                                const int gy = a + q, gx = x0 - R + xl;
-                                const bool rowok = gy >= lo && gy < hi && (p.border != 2 || (gy >= 0 && gy < p.height));
-                                const bool va = rowok && (p.border != 2 || (gx >= 0 && gx < p.width));
-                                const bool vb = rowok && (p.border != 2 || (gx + 1 >= 0 && gx + 1 < p.width));
-                                const float* fp = fs + q * FSW + xoff + xl;
-                                const float2 f = make_float2(va ? fp[0] : 0.f, vb ? fp[1] : 0.f);
-                                float* fr = fring + (blk * kQ + q) * kTW + (xl - R);
-                                if (xl >= R && xl < R + kTW) fr[0] = f.x;
-                                if (xl + 1 >= R && xl + 1 < R + kTW) fr[1] = f.y;
-                                float4* gp = reinterpret_cast<float4*>(gen + q * GS + xl);
-                                if (zk) gp[0] = make_float4(f.x, va ? 1.f : 0.f, f.y, vb ? 1.f : 0.f);
-                                if (NKR > 0) {
-                                    const CS2 c1 = harmonic1x2(f, p.inv_period);
-                                    const float2 nws = make_float2(-c1.s.x, -c1.s.y);
-                                    CS2 cs = harmonic_first2(c1, p.k_first);
-                                    if (!va) cs.c.x = cs.s.x = 0.f;
-                                    if (!vb) cs.c.y = cs.s.y = 0.f;
-                                    float4* gk = gp + (size_t)zk * kQ * GS / 2;
-#pragma unroll
-                                    for (int kk = 0; kk < NKR; ++kk) {
-                                        const float2 cf = __fmul2_rn(cs.c, f), sf = __fmul2_rn(cs.s, f);
-                                        gk[(size_t)(2 * kk) * kQ * GS / 2] = make_float4(cf.x, sf.x, cf.y, sf.y);
-                                        gk[(size_t)(2 * kk + 1) * kQ * GS / 2] = make_float4(cs.c.x, cs.s.x, cs.c.y, cs.s.y);
-                                        if (kk + 1 < NKR) cs = rotate2(cs, c1, nws);
-                                    }
-                                }
-                            }
-                        }
-                    }
-                }
-                FBF_PHASE(4);
-                named_sync(1, nrole);  // gen complete (and fstage[fb] fully read)
-                if (tid == 0) mbar_arrive(&fs_empty[fb]);
-                FBF_PHASE(5);
-
-                // ---- row pass: horizontal taps into ring block blk -------------
-                {  // nrole == np * kItemsPerPair: one item per producer thread
-                    const int q = tid % kQ;
-                    const int xc = (tid / kQ) % (kTW / kP);
-                    const int pr = tid / (kQ * (kTW / kP));
-                    const float4* gin = reinterpret_cast<const float4*>(gen + ((size_t)pr * kQ + q) * GS + xc * kP);
+                {   // horizontal pass: lane = (row q, 8-column chunk xc)
+                    const int q = lane % kQ;
+                    const int xc = lane / kQ;
+                    static_assert(kQ * (kTW / kP) == 32, "one pair = one warp of row items");
+                    const float4* gin = reinterpret_cast<const float4*>(gen + (((size_t)gb * np + pr) * kQ + q) * GS + xc * kP);
                     float2 accp[kP];
 #pragma unroll
                     for (int o = 0; o < kP; ++o) accp[o] = make_float2(0.f, 0.f);
@@ -528,117 +659,30 @@ __global__ void __launch_bounds__(2 * (1 + 2 * NKR) * kItemsPerPair + 32, (block
                             }
                         }
                     }
-                    float4* hout =
-                        reinterpret_cast<float4*>(ring + ((size_t)pr * RROWS + blk * kQ + q) * RS + xc * kP);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&gen_empty[gb]);  // this warp's gen rows consumed
+                    float4* hout = reinterpret_cast<float4*>(myring + ((size_t)blk * kQ + q) * RS + xc * kP);
 #pragma unroll
                     for (int o = 0; o < kP / 2; ++o)
                         hout[o] = make_float4(accp[2 * o].x, accp[2 * o].y, accp[2 * o + 1].x, accp[2 * o + 1].y);
                 }
                 FBF_PHASE(6);
-                named_sync(1, nrole);                       // every row of block blk written; gen free
-                if (tid == 0) mbar_arrive(&full_bar[blk]);  // release to the consumer
+                __syncwarp();  // the warp's ring block is complete
+                // column buffer cb must have been consumed by COMB even on warm-up steps:
+                // the arrival below completes a phase of col_full[cb], and a warp running
+                // ahead must not complete the phase of a step its siblings have not finished
+                if (g >= NCB) mbar_wait(&col_empty[cb], (unsigned)((g / NCB - 1) & 1));
                 FBF_PHASE(7);
-            }
-        } else {
-            // =========================== CONSUMER ===========================
-            float* dst = p.dst + (long long)frame * p.dst_frame_stride;
-            float2* acc = p.acc ? p.acc + (long long)frame * p.acc_frame_stride : nullptr;
-            FBF_PHASE_T0();
-            for (int s = 0; s < steps; ++s) {
-                const int g = gstep + s;
-                const int blk = g % RBX;
-                const int a = a0 + s * kQ;
-                FBF_PHASE(8);
-                mbar_wait(&full_bar[blk], (unsigned)((g / RBX) & 1));
-                FBF_PHASE(9);
-                if (s >= s0) {  // warm-up steps only fill the ring
-                    // ---- column pass: vertical taps over the ring -> colout ----
-                    {
-                        const int x = tid % kTW;
-                        const int grp = (tid / kTW) % (kQ / kP);  // warp-uniform row group
-                        const int pr = tid / (kTW * (kQ / kP));
-                        const float2* rp = ring + (size_t)pr * RROWS * RS;
-                        float2* oc = reinterpret_cast<float2*>(reinterpret_cast<float*>(colout) +
-                                                               (size_t)pr * kQ * 2 * kTW + x);
-                        if (kQ / kP == 1 || grp == 0)
-                            column_pass<R, 0>(rp, blk, x, p.taps, oc);
-                        else
-                            column_pass<R, (kQ / kP > 1 ? kP : 0)>(rp, blk, x, p.taps, oc);
-                    }
+                if (s >= s0) {
+                    // vertical pass: lane = column x, the step's Q output rows
+                    static_assert(kQ == kP, "one column item per lane");
+                    column_pass<R, 0>(myring, blk, lane, p.taps,
+                                      colout + ((size_t)cb * np + pr) * kQ * 2 * kTW + lane);
                     FBF_PHASE(10);
-                    named_sync(2, nrole);
-                    FBF_PHASE(11);
-
-                    // ---- combine -----------------------------------------------
-                    // one item = two adjacent output pixels, packed FP32 math
-                    constexpr int HTW = kTW / 2;
-                    constexpr int CITER = NKR > 0 ? (kQ * HTW + 2 * NKR * kItemsPerPair - 1) / (2 * NKR * kItemsPerPair) : 4;
-#pragma unroll
-                    for (int it = 0; it < CITER; ++it) {
-                        const int item = it * nrole + tid;
-                        const int q = item / HTW, x = 2 * (item - q * HTW);
-                        const int y = a - R + q, gxo = x0 + x;
-                        if (item >= kQ * HTW || y >= yb || gxo >= p.width) continue;
-                        const bool vb = gxo + 1 < p.width;
-                        int frow = blk * kQ + q - R;
-                        while (frow < 0) frow += RROWS;
-                        const float2 f = *reinterpret_cast<const float2*>(fring + frow * kTW + x);
-                        float2 num = make_float2(0.f, 0.f), den = make_float2(0.f, 0.f);
-                        const long long ai = (long long)(y - p.out_row0) * p.width + gxo;
-                        if (!p.first_chunk) {
-                            const float2 nda = acc[ai], ndb = vb ? acc[ai + 1] : make_float2(0.f, 0.f);
-                            num = make_float2(nda.x, ndb.x);
-                            den = make_float2(nda.y, ndb.y);
-                        }
-                        // planar colout: [pair][q][component][TW]
-                        const float* go = reinterpret_cast<const float*>(colout) + q * 2 * kTW + x;
-                        constexpr int PSTR = kQ * 2 * kTW;  // floats per pair
-                        if (zk) {
-                            const float2 gx0 = *reinterpret_cast<const float2*>(go);
-                            const float2 gy0 = *reinterpret_cast<const float2*>(go + kTW);
-                            const float2 c0 = make_float2(p.coeff[0], p.coeff[0]);
-                            num = __ffma2_rn(c0, gx0, num);
-                            den = __ffma2_rn(c0, gy0, den);
-                        }
-                        if (NKR > 0) {
-                            const CS2 c1 = harmonic1x2(f, p.inv_period);
-                            const float2 nws = make_float2(-c1.s.x, -c1.s.y);
-                            CS2 cs = harmonic_first2(c1, p.k_first);
-                            const float* gk = go + zk * PSTR;
-#pragma unroll
-                            for (int kk = 0; kk < NKR; ++kk) {
-                                const float2 ck = make_float2(p.coeff[zk + kk], p.coeff[zk + kk]);
-                                const float* gn = gk + (2 * kk) * PSTR;
-                                const float* gd = gk + (2 * kk + 1) * PSTR;
-                                const float2 gnx = *reinterpret_cast<const float2*>(gn);
-                                const float2 gny = *reinterpret_cast<const float2*>(gn + kTW);
-                                const float2 gdx = *reinterpret_cast<const float2*>(gd);
-                                const float2 gdy = *reinterpret_cast<const float2*>(gd + kTW);
-                                num = __ffma2_rn(ck, __ffma2_rn(cs.s, gny, __fmul2_rn(cs.c, gnx)), num);
-                                den = __ffma2_rn(ck, __ffma2_rn(cs.s, gdy, __fmul2_rn(cs.c, gdx)), den);
-                                if (kk + 1 < NKR) cs = rotate2(cs, c1, nws);
-                            }
-                        }
-                        float* drow = dst + (long long)(y - p.out_row0) * p.dst_pitch + gxo;
-                        if (p.last_chunk) {
-                            float oa = f.x, ob = f.y;
-                            unsigned nfb = 0;
-                            if (den.x > 1e-12f) oa = __fdividef(num.x, den.x); else ++nfb;
-                            if (den.y > 1e-12f) ob = __fdividef(num.y, den.y); else nfb += vb;
-                            if (nfb) atomicAdd(s_fallbacks, nfb);
-                            drow[0] = oa;
-                            if (vb) drow[1] = ob;
-                        } else {
-                            acc[ai] = make_float2(num.x, den.x);
-                            if (vb) acc[ai + 1] = make_float2(num.y, den.y);
-                        }
-                    }
+                    __syncwarp();
                 }
-                FBF_PHASE(12);
-                named_sync(2, nrole);  // all consumer reads of the ring / colout done
-                FBF_PHASE(13);
-                // the oldest block of this step's window is no longer needed
-                if (tid == 0 && g - RB + 1 >= 0) mbar_arrive(&empty_bar[(g - RB + 1) % RBX]);
+                if (lane == 0) mbar_arrive(&col_full[cb]);  // (warm-up steps hand over nothing)
+                FBF_PHASE(11);
             }
         }
         gstep += steps;
@@ -649,8 +693,8 @@ __global__ void __launch_bounds__(2 * (1 + 2 * NKR) * kItemsPerPair + 32, (block
         unsigned long long _gt1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_gt1));
         atomicMax(&g_phase_cycles[14], (unsigned long long)(clock64() - _cta_t0));
-        if (blockIdx.x < 1024) g_cta_cycles[blockIdx.x] = (unsigned long long)(clock64() - _cta_t0);
         atomicAdd(&g_phase_cycles[15], (unsigned long long)(clock64() - _cta_t0) * 1000ull / (_gt1 - _gt0 + 1));
+        if (blockIdx.x < 1024) g_cta_cycles[blockIdx.x] = (unsigned long long)(clock64() - _cta_t0);
     }
 #endif
     if (threadIdx.x == 0 && p.fallbacks && *s_fallbacks) atomicAdd(p.fallbacks, (unsigned long long)*s_fallbacks);
@@ -667,7 +711,7 @@ cudaError_t launch_fused(const Params& p, int grid, cudaStream_t stream) {
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    fbf_fused_kernel<R, NKR><<<grid, 2 * p.n_pairs * kItemsPerPair + 32, smem, stream>>>(p);
+    fbf_fused_kernel<R, NKR><<<grid, kRoles * p.n_pairs * kItemsPerPair + kExtraThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 

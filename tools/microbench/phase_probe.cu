@@ -35,10 +35,10 @@ int main(int argc, char** argv) {
   }
   std::sort(tms.begin(), tms.end()); float ms = tms[10];
   unsigned long long r[16]; cudaMemcpyFromSymbol(r, g_phase_cycles, sizeof r);
-  int occ=0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fbf_fused_kernel<15,3>, 2*7*kItemsPerPair+32, Geometry<15>::smem_bytes(7)); printf("occupancy %d blocks/SM\n", occ);
+  int occ=0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fbf_fused_kernel<15,3>, kRoles*7*kItemsPerPair+kExtraThreads, Geometry<15>::smem_bytes(7)); printf("occupancy %d blocks/SM\n", occ);
   printf("grid %d: %.3f ms (%s)\n", grid, ms, cudaGetErrorString(cudaGetLastError()));
-  const char* names[16] = {"P:loop/arrive", "P:fs wait", "-", "P:empty wait", "P:gen", "P:sync after gen",
-                           "P:row", "P:sync+arrive", "C:loop", "C:full wait", "C:col", "C:sync after col", "C:combine", "C:end sync", "", ""};
+  const char* names[16] = {"G:loop", "G:waits", "P:loop", "P:gen wait", "G:gen", "G:arrive",
+                           "P:row", "P:colbuf wait", "-", "-", "P:col", "P:arrive", "C:wait", "C:combine", "", ""};
   double tp = 0, tc = 0; for (int i = 0; i < 8; i++) tp += r[i]; for (int i = 8; i < 14; i++) tc += r[i];
   printf("max CTA cycles %llu (%.3f ms at 1965 MHz); mean SM clock in kernel %.0f MHz; mean per-step (115) %.0f\n", r[14], r[14] / 1.965e6, (double)r[15] / grid, (double)r[14] / 115);
   { unsigned long long cc[1024]; cudaMemcpyFromSymbol(cc, g_cta_cycles, sizeof cc);
