@@ -104,7 +104,10 @@ int cuda_fail(cudaError_t e, const char* what) {
 struct DeviceCtx {
     int device = 0;
     int num_sms = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;      // compute
+    cudaStream_t stream_in = nullptr;   // host -> device copies
+    cudaStream_t stream_out = nullptr;  // device -> host copies
+    std::vector<cudaEvent_t> events;    // pipelining pool
     std::mutex mtx;
     void* arena = nullptr;  // cached device scratch
     size_t arena_bytes = 0;
@@ -116,8 +119,19 @@ struct DeviceCtx {
         FBF_CUDA(cudaSetDevice(dev), "cudaSetDevice");
         FBF_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev), "attr");
         FBF_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        FBF_CUDA(cudaStreamCreateWithFlags(&stream_in, cudaStreamNonBlocking), "cudaStreamCreate");
+        FBF_CUDA(cudaStreamCreateWithFlags(&stream_out, cudaStreamNonBlocking), "cudaStreamCreate");
         FBF_CUDA(cudaMalloc(&d_counters, 2 * sizeof(unsigned long long)), "cudaMalloc counters");
         FBF_CUDA(cudaMallocHost(&h_counters, 2 * sizeof(unsigned long long)), "cudaMallocHost");
+        return FBF_OK;
+    }
+    int event(size_t i, cudaEvent_t* ev) {
+        while (events.size() <= i) {
+            cudaEvent_t e;
+            FBF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            events.push_back(e);
+        }
+        *ev = events[i];
         return FBF_OK;
     }
     int reserve(size_t bytes) {
@@ -236,7 +250,8 @@ struct Job {
 // Runs every chunk launch for one job on `stream`. `scratch` must hold
 // n_frames * out_rows * width float2 when K needs more than one chunk.
 int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int border,
-            float2* scratch, unsigned long long* d_fallbacks, cudaStream_t stream) {
+            float2* scratch, unsigned long long* d_fallbacks, cudaStream_t stream,
+            unsigned int* d_bad = nullptr) {
     const int r = (int)std::ceil(3.0 * theta);
     const auto& ent = fbf_dev::radius_entry(r);
     const Plan plan = make_plan(a.K, r);
@@ -254,6 +269,8 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
     p.acc = plan.chunks.size() > 1 ? scratch : nullptr;
     p.acc_frame_stride = (long long)job.out_rows * job.width;
     p.fallbacks = d_fallbacks;
+    p.bad_pixels = d_bad;
+    p.range_max = (float)a.R;
     p.width = job.width;
     p.height = job.height;
     p.n_frames = job.n_frames;
@@ -306,7 +323,15 @@ size_t scratch_bytes(const Approx& a, double theta, size_t pixels) {
 
 size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
-// Host-buffer path for n_frames frames on one device (H2D, validate, filter, D2H).
+void source_window(int height, int out_row0, int out_rows, int r, int border, int* row0, int* rows);
+int extent_of(bool bands, int height, int n_frames) { return bands ? height : n_frames; }
+
+// Host-buffer path for n_frames frames on one device. The work is cut into
+// pieces (row bands of a single large image, or groups of frames) and
+// pipelined over three streams: H2D of piece i+1 and D2H of piece i-1 overlap
+// the kernel of piece i; intensity validation is fused into the kernel. Bands read the full device image, so their
+// halos need no extra copies: a band's kernel waits for the copy of the last
+// chunk its border-mapped window reaches. Results are identical to one launch.
 int filter_frames_on_device(int dev, const float* img, int n_frames, int width, int height, double theta,
                             const Approx& a, int border, float* out, long long* fallbacks) {
     DeviceCtx* ctx = nullptr;
@@ -314,7 +339,8 @@ int filter_frames_on_device(int dev, const float* img, int n_frames, int width, 
     if (rc != FBF_OK) return rc;
     std::lock_guard<std::mutex> lock(ctx->mtx);
     FBF_CUDA(cudaSetDevice(dev), "cudaSetDevice");
-    const size_t pixels = (size_t)n_frames * width * height;
+    const size_t fp = (size_t)width * height;
+    const size_t pixels = (size_t)n_frames * fp;
     const size_t img_bytes = align_up(pixels * sizeof(float));
     const size_t scr = align_up(scratch_bytes(a, theta, pixels));
     rc = ctx->reserve(2 * img_bytes + scr);
@@ -322,20 +348,58 @@ int filter_frames_on_device(int dev, const float* img, int n_frames, int width, 
     float* d_in = (float*)ctx->arena;
     float* d_out = (float*)((char*)ctx->arena + img_bytes);
     float2* d_scr = scr ? (float2*)((char*)ctx->arena + 2 * img_bytes) : nullptr;
-    cudaStream_t st = ctx->stream;
-    FBF_CUDA(cudaMemsetAsync(ctx->d_counters, 0, 2 * sizeof(unsigned long long), st), "memset");
-    FBF_CUDA(cudaMemcpyAsync(d_in, img, pixels * sizeof(float), cudaMemcpyHostToDevice, st), "H2D");
-    fbf_dev::validate_kernel<<<ctx->num_sms * 4, 256, 0, st>>>(d_in, pixels, (float)a.R,
-                                                              (unsigned int*)(ctx->d_counters + 1));
-    FBF_CUDA(cudaGetLastError(), "validate launch");
-    Job job{d_in, (long long)width * height, 0, height, d_out, (long long)width * height,
-            width, height, n_frames, 0, height};
-    rc = run_job(*ctx, job, theta, a, border, d_scr, ctx->d_counters, st);
-    if (rc != FBF_OK) return rc;
-    FBF_CUDA(cudaMemcpyAsync(out, d_out, pixels * sizeof(float), cudaMemcpyDeviceToHost, st), "D2H");
+    cudaStream_t sc = ctx->stream, si = ctx->stream_in, so = ctx->stream_out;
+    unsigned int* d_flag = (unsigned int*)(ctx->d_counters + 1);
+    const int r = (int)std::ceil(3.0 * theta);
+    FBF_CUDA(cudaMemsetAsync(ctx->d_counters, 0, 2 * sizeof(unsigned long long), si), "memset");
+
+    // piece i covers rows [rows0[i], rows0[i+1]) of a single image, or frames [f0, f1)
+    const bool bands = n_frames == 1;
+    int pieces = bands ? (int)std::min<long long>(8, std::max<long long>(1, (long long)pixels / (1 << 19)))
+                       : std::min(n_frames, 16);
+    if (bands) pieces = std::max(1, std::min(pieces, height / std::max(64, 4 * r)));
+    static const int forced_pieces = [] {
+        const char* e = std::getenv("FBF_PIECES");  // tuning override
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced_pieces > 0) pieces = std::max(1, std::min(forced_pieces, extent_of(bands, height, n_frames)));
+    std::vector<int> lo(pieces + 1);
+    const int extent = bands ? height : n_frames;
+    for (int i = 0; i <= pieces; ++i) lo[i] = (int)((long long)extent * i / pieces);
+    const size_t unit = bands ? (size_t)width : fp;  // floats per row / per frame
+    cudaEvent_t ev;
+    for (int i = 0; i < pieces; ++i) {
+        const size_t off = (size_t)lo[i] * unit, n = (size_t)(lo[i + 1] - lo[i]) * unit;
+        FBF_CUDA(cudaMemcpyAsync(d_in + off, img + off, n * sizeof(float), cudaMemcpyHostToDevice, si), "H2D");
+        if ((rc = ctx->event(2 * i, &ev)) != FBF_OK) return rc;
+        FBF_CUDA(cudaEventRecord(ev, si), "event");
+    }
+    for (int i = 0; i < pieces; ++i) {
+        int need = i;  // last input piece this piece's window reaches
+        if (bands) {
+            int s0 = 0, sn = 0;
+            source_window(height, lo[i], lo[i + 1] - lo[i], r, border, &s0, &sn);
+            while (need + 1 < pieces && lo[need + 1] < s0 + sn) ++need;
+        }
+        if ((rc = ctx->event(2 * need, &ev)) != FBF_OK) return rc;
+        FBF_CUDA(cudaStreamWaitEvent(sc, ev, 0), "wait");
+        Job job = bands ? Job{d_in, (long long)fp, 0, height, d_out + (size_t)lo[i] * width, (long long)fp,
+                              width, height, 1, lo[i], lo[i + 1] - lo[i]}
+                        : Job{d_in + (size_t)lo[i] * fp, (long long)fp, 0, height, d_out + (size_t)lo[i] * fp,
+                              (long long)fp, width, height, lo[i + 1] - lo[i], 0, height};
+        float2* sp = d_scr ? d_scr + (size_t)lo[i] * unit : nullptr;
+        // intensity validation runs inside the kernel (every pixel is combined once)
+        rc = run_job(*ctx, job, theta, a, border, sp, ctx->d_counters, sc, d_flag);
+        if (rc != FBF_OK) return rc;
+        if ((rc = ctx->event(2 * i + 1, &ev)) != FBF_OK) return rc;
+        FBF_CUDA(cudaEventRecord(ev, sc), "event");
+        FBF_CUDA(cudaStreamWaitEvent(so, ev, 0), "wait");
+        const size_t off = (size_t)lo[i] * unit, n = (size_t)(lo[i + 1] - lo[i]) * unit;
+        FBF_CUDA(cudaMemcpyAsync(out + off, d_out + off, n * sizeof(float), cudaMemcpyDeviceToHost, so), "D2H");
+    }
     FBF_CUDA(cudaMemcpyAsync(ctx->h_counters, ctx->d_counters, 2 * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, st), "D2H counters");
-    FBF_CUDA(cudaStreamSynchronize(st), "filter");
+                             cudaMemcpyDeviceToHost, so), "D2H counters");
+    FBF_CUDA(cudaStreamSynchronize(so), "filter");
     if (ctx->h_counters[1]) return fail(FBF_ERANGE, "filter: pixel intensity outside [0, R]");
     if (fallbacks) *fallbacks += (long long)ctx->h_counters[0];
     return FBF_OK;
@@ -564,11 +628,9 @@ int fbf_fast_bilateral_bands_f32(const float* img, int width, int height, double
         FBF_CUDA(cudaMemsetAsync(ctx->d_counters, 0, 2 * sizeof(unsigned long long), st), "memset");
         FBF_CUDA(cudaMemcpyAsync(d_in, img + (size_t)s0 * width, (size_t)sn * width * sizeof(float),
                                  cudaMemcpyHostToDevice, st), "H2D band");
-        fbf_dev::validate_kernel<<<ctx->num_sms * 4, 256, 0, st>>>(d_in, (size_t)sn * width, (float)a.R,
-                                                                  (unsigned int*)(ctx->d_counters + 1));
-        FBF_CUDA(cudaGetLastError(), "validate launch");
         Job job{d_in, 0, s0, sn, d_out, 0, width, height, 1, y0, y1 - y0};
-        rc2 = run_job(*ctx, job, theta, a, border, d_scr, ctx->d_counters, st);
+        rc2 = run_job(*ctx, job, theta, a, border, d_scr, ctx->d_counters, st,
+                      (unsigned int*)(ctx->d_counters + 1));  // validation fused into the combine
         if (rc2 != FBF_OK) return rc2;
         FBF_CUDA(cudaMemcpyAsync(out + (size_t)y0 * width, d_out, (size_t)(y1 - y0) * width * sizeof(float),
                                  cudaMemcpyDeviceToHost, st), "D2H band");

@@ -94,6 +94,8 @@ struct Params {
     float2* acc;                 // (num, den) scratch for multi-chunk runs, pitch = width
     long long acc_frame_stride;
     unsigned long long* fallbacks;  // device counter (may be null)
+    unsigned int* bad_pixels;    // set to 1 if any output pixel's f is non-finite or outside [0, range_max]
+    float range_max;             // R (filter.cpp:19-23 validation, fused into the combine)
     int width, height, n_frames, border;
     int out_row0, out_rows;
     int k_lo, n_pairs;           // chunk: k in [k_lo, k_lo + (k_lo == 0) + NKR)
@@ -113,10 +115,14 @@ struct Geometry {
     static constexpr int GS = GW + ((2 - GW % 4) + 4) % 4;       // gen stride (float2), GS/2 odd
     static constexpr int FSW = (GW + 3 + 3) / 4 * 4;             // f staging row: GW + 16B-alignment slack
     static constexpr int RB = 1 + (2 * R + kQ - 1) / kQ;         // ring blocks a column pass reads
-    static constexpr int RROWS = RB * kQ;                        // ring rows (private to a pair warp)
+    static constexpr int RBP = RB + 1;                           // + the block the next row pass writes
+    static constexpr int RROWS = RBP * kQ;                       // ring rows (private to a pair warp)
     static constexpr int RS = kTW + 2;                           // ring stride (float2), RS/2 odd
     static constexpr int NFS = 3;                                // f staging buffers (loader runs ahead)
-    static constexpr int NGB = 2;                                // gen buffers (gen runs ahead)
+#ifndef FBF_NGB
+#define FBF_NGB 2
+#endif
+    static constexpr int NGB = FBF_NGB;                          // gen buffers (gen runs ahead)
     static constexpr int NCB = 2;                                // column-result buffers
     static constexpr size_t fstage_bytes = sizeof(float) * NFS * kQ * FSW;  // multiple of 128
     static constexpr size_t bar_bytes = 8 * (2 * NFS + 2 * NGB + 2 * NCB) + 8;  // mbarriers + counter
@@ -314,6 +320,81 @@ __device__ __forceinline__ void column_pass(const float2* __restrict__ ring_pair
     }
 }
 
+// One software-pipelined pair-warp iteration: the horizontal pass of step t
+// (DO_ROW; lane = (row q, 8-column chunk)) interleaved with the vertical pass of
+// step t-1 (DO_COL; lane = column). The two FFMA2 streams are independent, so each
+// hides the other's shared-memory latency. Row loads: (8+2R)/2 float4, column
+// loads: 8+2R float2 -- always 2 column rows per row chunk.
+template <int R, bool DO_ROW, bool DO_COL>
+__device__ __forceinline__ void pair_iter(const float4* __restrict__ gin, float2* ring_pair, int blk_row,
+                                          int blk_col, int lane, const float* taps, float* out_col,
+                                          uint64_t* gen_empty_bar) {
+    using G = Geometry<R>;
+    constexpr int RB = G::RB, RBP = G::RBP, RS = G::RS;
+    const int q = lane % kQ, xc = lane / kQ;
+    float2 accr[kP], accc[kP];
+    const float2* bptr[RB];
+#pragma unroll
+    for (int o = 0; o < kP; ++o) {
+        accr[o] = make_float2(0.f, 0.f);
+        accc[o] = make_float2(0.f, 0.f);
+    }
+    if (DO_COL) {
+#pragma unroll
+        for (int b = 0; b < RB; ++b) {  // bptr[b] = block (blk_col - b) mod RBP
+            int bb = blk_col - b;
+            bb += bb < 0 ? RBP : 0;
+            bptr[b] = ring_pair + bb * kQ * RS + lane;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < (kP + 2 * R) / 2; ++j) {
+        if (DO_ROW) {
+            const float4 v4 = gin[j];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int jj = 2 * j + h;
+                const float2 v = h ? make_float2(v4.z, v4.w) : make_float2(v4.x, v4.y);
+#pragma unroll
+                for (int o = 0; o < kP; ++o) {
+                    const int d = jj - o;  // tap index 0..2R, ascending per output
+                    if (d >= 0 && d <= 2 * R) accr[o] = ffma2(v, taps[d >= R ? d - R : R - d], accr[o]);
+                }
+            }
+        }
+        if (DO_COL) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = 2 * j + h;
+                const int jr = i - 2 * R;                       // window row, compile-time
+                const int b = jr >= 0 ? 0 : (-jr + kQ - 1) / kQ;  // blocks back
+                const float2 v = bptr[b][(jr + b * kQ) * RS];
+#pragma unroll
+                for (int o = 0; o < kP; ++o) {
+                    const int d = i - o;
+                    if (d >= 0 && d <= 2 * R) accc[o] = ffma2(v, taps[d >= R ? d - R : R - d], accc[o]);
+                }
+            }
+        }
+    }
+    if (DO_ROW) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(gen_empty_bar);  // this warp's gen rows consumed
+        float4* hout = reinterpret_cast<float4*>(ring_pair + ((size_t)blk_row * kQ + q) * RS + xc * kP);
+#pragma unroll
+        for (int o = 0; o < kP / 2; ++o)
+            hout[o] = make_float4(accr[2 * o].x, accr[2 * o].y, accr[2 * o + 1].x, accr[2 * o + 1].y);
+    }
+    if (DO_COL) {
+#pragma unroll
+        for (int o = 0; o < kP; ++o) {  // planar: [q][component][TW]
+            float* oc = out_col + o * 2 * kTW + lane;
+            oc[0] = accc[o].x;
+            oc[kTW] = accc[o].y;
+        }
+    }
+}
+
 // Warp roles (np = channel pairs of the launch):
 //   PAIR (np warps) : warp p owns channel pair p: horizontal pass of the step's
 //                     Q rows into ITS OWN ring, then the vertical pass of the step
@@ -334,7 +415,7 @@ template <int R, int NKR>
 __global__ void __launch_bounds__(kRoles * (1 + 2 * NKR) * kItemsPerPair + kExtraThreads, 1)
     fbf_fused_kernel(const __grid_constant__ Params p) {
     using G = Geometry<R>;
-    constexpr int GW = G::GW, GS = G::GS, FSW = G::FSW, RB = G::RB, RROWS = G::RROWS, RS = G::RS;
+    constexpr int GW = G::GW, GS = G::GS, FSW = G::FSW, RB = G::RB, RBP = G::RBP, RROWS = G::RROWS, RS = G::RS;
     constexpr int NFS = G::NFS, NGB = G::NGB, NCB = G::NCB;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int np = p.n_pairs;
@@ -462,6 +543,9 @@ __global__ void __launch_bounds__(kRoles * (1 + 2 * NKR) * kItemsPerPair + kExtr
         const bool vb = gxo + 1 < p.width;
         const float* srow = p.src + (long long)sg.frame * p.src_frame_stride + (long long)(y - p.src_row0) * p.src_pitch;
         const float2 f = make_float2(__ldg(srow + gxo), vb ? __ldg(srow + gxo + 1) : 0.f);
+        // validate_intensities (filter.cpp:19-23): every pixel is an output pixel exactly once
+        if (p.bad_pixels && !(f.x >= 0.f && f.x <= p.range_max && f.y >= 0.f && f.y <= p.range_max))
+            atomicOr(p.bad_pixels, 1u);
         float* dst = p.dst + (long long)sg.frame * p.dst_frame_stride;
         float2* acc = p.acc ? p.acc + (long long)sg.frame * p.acc_frame_stride : nullptr;
         float2 num = make_float2(0.f, 0.f), den = make_float2(0.f, 0.f);
@@ -626,62 +710,36 @@ __global__ void __launch_bounds__(kRoles * (1 + 2 * NKR) * kItemsPerPair + kExtr
             }
         } else {
             // ============================= PAIR =============================
+            // iteration t: horizontal pass of step t + vertical pass of step t - 1
             const int pr = tid / 32;  // this warp's channel pair
             float2* myring = ring + (size_t)pr * RROWS * RS;
+            static_assert(kQ * (kTW / kP) == 32 && kQ == kP, "one pair = one warp");
             FBF_PHASE_T0();
-            for (int s = 0; s < steps; ++s) {
-                const int g = gstep + s;
-                const int gb = g % NGB, cb = g % NCB;
-                const int blk = g % RB;  // this step's ring block (this warp's private ring)
+            for (int t = 0; t <= steps; ++t) {
+                const bool do_row = t < steps;
+                const bool do_col = t >= 1 + s0;
+                const int g = gstep + t, gc = g - 1;
+                const int gb = g % NGB, cb = gc % NCB;
                 FBF_PHASE(2);
-                mbar_wait(&gen_full[gb], (unsigned)((g / NGB) & 1));
-                FBF_PHASE(3);
-                {   // horizontal pass: lane = (row q, 8-column chunk xc)
-                    const int q = lane % kQ;
-                    const int xc = lane / kQ;
-                    static_assert(kQ * (kTW / kP) == 32, "one pair = one warp of row items");
-                    const float4* gin = reinterpret_cast<const float4*>(gen + (((size_t)gb * np + pr) * kQ + q) * GS + xc * kP);
-                    float2 accp[kP];
-#pragma unroll
-                    for (int o = 0; o < kP; ++o) accp[o] = make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int j = 0; j < (kP + 2 * R) / 2; ++j) {
-                        const float4 v4 = gin[j];
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int jj = 2 * j + h;
-                            const float2 v = h ? make_float2(v4.z, v4.w) : make_float2(v4.x, v4.y);
-#pragma unroll
-                            for (int o = 0; o < kP; ++o) {
-                                const int d = jj - o;  // tap index 0..2R, ascending per output
-                                if (d >= 0 && d <= 2 * R)
-                                    accp[o] = ffma2(v, p.taps[d >= R ? d - R : R - d], accp[o]);
-                            }
-                        }
-                    }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&gen_empty[gb]);  // this warp's gen rows consumed
-                    float4* hout = reinterpret_cast<float4*>(myring + ((size_t)blk * kQ + q) * RS + xc * kP);
-#pragma unroll
-                    for (int o = 0; o < kP / 2; ++o)
-                        hout[o] = make_float4(accp[2 * o].x, accp[2 * o].y, accp[2 * o + 1].x, accp[2 * o + 1].y);
-                }
-                FBF_PHASE(6);
-                __syncwarp();  // the warp's ring block is complete
+                if (do_row) mbar_wait(&gen_full[gb], (unsigned)((g / NGB) & 1));
                 // column buffer cb must have been consumed by COMB even on warm-up steps:
                 // the arrival below completes a phase of col_full[cb], and a warp running
                 // ahead must not complete the phase of a step its siblings have not finished
-                if (g >= NCB) mbar_wait(&col_empty[cb], (unsigned)((g / NCB - 1) & 1));
-                FBF_PHASE(7);
-                if (s >= s0) {
-                    // vertical pass: lane = column x, the step's Q output rows
-                    static_assert(kQ == kP, "one column item per lane");
-                    column_pass<R, 0>(myring, blk, lane, p.taps,
-                                      colout + ((size_t)cb * np + pr) * kQ * 2 * kTW + lane);
-                    FBF_PHASE(10);
-                    __syncwarp();
-                }
-                if (lane == 0) mbar_arrive(&col_full[cb]);  // (warm-up steps hand over nothing)
+                if (t >= 1 && gc >= NCB) mbar_wait(&col_empty[cb], (unsigned)((gc / NCB - 1) & 1));
+                FBF_PHASE(3);
+                const float4* gin = reinterpret_cast<const float4*>(
+                    gen + (((size_t)gb * np + pr) * kQ + lane % kQ) * GS + (lane / kQ) * kP);
+                float* oc = colout + ((size_t)cb * np + pr) * kQ * 2 * kTW;
+                const int blk_row = g % RBP, blk_col = gc % RBP;
+                if (do_row && do_col)
+                    pair_iter<R, true, true>(gin, myring, blk_row, blk_col, lane, p.taps, oc, &gen_empty[gb]);
+                else if (do_row)
+                    pair_iter<R, true, false>(gin, myring, blk_row, blk_col, lane, p.taps, oc, &gen_empty[gb]);
+                else if (do_col)
+                    pair_iter<R, false, true>(gin, myring, blk_row, blk_col, lane, p.taps, oc, &gen_empty[gb]);
+                FBF_PHASE(6);
+                __syncwarp();  // ring block / column results of this warp complete
+                if (t >= 1 && lane == 0) mbar_arrive(&col_full[cb]);  // (warm-up steps hand over nothing)
                 FBF_PHASE(11);
             }
         }
