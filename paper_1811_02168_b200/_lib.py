@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfbf.so")
+LIB_PATH = os.environ.get("FBF_LIB") or os.path.join(HERE, "libfbf.so")  # FBF_LIB: dev builds
 
 FBF_OK = 0
 FBF_EINVAL = 1

@@ -57,46 +57,61 @@ def _run(cmd: list[str], log: str) -> None:
         raise RuntimeError(f"build failed: {' '.join(cmd)}\n{p.stdout}{p.stderr}")
 
 
-def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False, out: str | None = None,
+          defines: list[str] | None = None, radius: int | None = None) -> str:
+    """Builds libfbf.so. Dev options: `out` (another library path), `defines`
+    (extra -D macros, e.g. FBF_SKIP_GEN), `radius` (specialise one radius only)."""
+    lib = out or LIB
     deps = _deps()
-    if not force and not _stale(LIB, deps):
-        return LIB
-    os.makedirs(BUILD, exist_ok=True)
+    if not force and not _stale(lib, deps):
+        return lib
+    extra = [f"-D{d}" for d in (defines or [])]
+    splits = RADIUS_SPLITS
+    build_dir = BUILD
+    if radius is not None:
+        splits = [(radius, radius)]
+        extra.append(f"-DFBF_DEV_RADIUS={radius}")
+    if out or defines or radius is not None:
+        build_dir = os.path.join(ROOT, "build", "fbf_dev_" + os.path.basename(lib).replace(".so", ""))
+    os.makedirs(build_dir, exist_ok=True)
     nvcc = _nvcc()
-    jobs = jobs or min(len(RADIUS_SPLITS) + 3, os.cpu_count() or 4)
+    jobs = jobs or min(len(splits) + 3, os.cpu_count() or 4)
     tasks = []
     objs = []
-    for lo, hi in RADIUS_SPLITS:
-        obj = os.path.join(BUILD, f"fbf_kernel_r{lo:02d}_{hi:02d}.o")
+    for lo, hi in splits:
+        obj = os.path.join(build_dir, f"fbf_kernel_r{lo:02d}_{hi:02d}.o")
         objs.append(obj)
-        tasks.append(([nvcc, *NVCC_FLAGS, f"-DFBF_R_LO={lo}", f"-DFBF_R_HI={hi}", "-c",
+        tasks.append(([nvcc, *NVCC_FLAGS, *extra, f"-DFBF_R_LO={lo}", f"-DFBF_R_HI={hi}", "-c",
                        os.path.join(CSRC, "fbf_kernel_inst.cu"), "-o", obj], obj + ".log"))
-    obj = os.path.join(BUILD, "fbf_api.o")
+    obj = os.path.join(build_dir, "fbf_api.o")
     objs.append(obj)
-    tasks.append(([nvcc, *NVCC_FLAGS, "-c", os.path.join(CSRC, "fbf_api.cu"), "-o", obj], obj + ".log"))
+    tasks.append(([nvcc, *NVCC_FLAGS, *extra, "-c", os.path.join(CSRC, "fbf_api.cu"), "-o", obj], obj + ".log"))
     for src in ("fbf_params.cpp", "fbf_synth.cpp"):
-        obj = os.path.join(BUILD, src.replace(".cpp", ".o"))
+        obj = os.path.join(build_dir, src.replace(".cpp", ".o"))
         objs.append(obj)
         tasks.append((["g++", *CXX_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj], obj + ".log"))
     with cf.ThreadPoolExecutor(jobs) as ex:
         futs = [ex.submit(_run, cmd, log) for cmd, log in tasks]
         for f in futs:
             f.result()
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lpthread"],
-         os.path.join(BUILD, "link.log"))
-    os.replace(tmp, LIB)
+         os.path.join(build_dir, "link.log"))
+    os.replace(tmp, lib)
     if verbose:
-        print(f"built {LIB}")
-    return LIB
+        print(f"built {lib}")
+    return lib
 
 
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--jobs", type=int, default=None)
+    ap.add_argument("--out", default=None, help="dev: library path (default: the in-tree libfbf.so)")
+    ap.add_argument("-D", dest="defines", action="append", default=[], help="dev: extra macro")
+    ap.add_argument("--radius", type=int, default=None, help="dev: specialise one radius only")
     a = ap.parse_args()
-    print(build(force=a.force, jobs=a.jobs, verbose=True))
+    print(build(force=a.force, jobs=a.jobs, verbose=True, out=a.out, defines=a.defines, radius=a.radius))
 
 
 if __name__ == "__main__":

@@ -29,38 +29,49 @@
 #include "fbf_kernel.cuh"
 
 namespace fbf_dev {
-#define FBF_EXTERN1(R, N) \
-    extern template cudaError_t launch_fused<R, N>(const Params&, int, cudaStream_t);
-#define FBF_EXTERN(R) \
-    FBF_EXTERN1(R, 0) FBF_EXTERN1(R, 1) FBF_EXTERN1(R, 2) FBF_EXTERN1(R, 3) FBF_EXTERN1(R, 4)
-FBF_EXTERN(1) FBF_EXTERN(2) FBF_EXTERN(3) FBF_EXTERN(4) FBF_EXTERN(5) FBF_EXTERN(6) FBF_EXTERN(7)
-FBF_EXTERN(8) FBF_EXTERN(9) FBF_EXTERN(10) FBF_EXTERN(11) FBF_EXTERN(12) FBF_EXTERN(13)
-FBF_EXTERN(14) FBF_EXTERN(15) FBF_EXTERN(16) FBF_EXTERN(17) FBF_EXTERN(18) FBF_EXTERN(19)
-FBF_EXTERN(20) FBF_EXTERN(21) FBF_EXTERN(22) FBF_EXTERN(23) FBF_EXTERN(24) FBF_EXTERN(25)
-FBF_EXTERN(26) FBF_EXTERN(27) FBF_EXTERN(28) FBF_EXTERN(29) FBF_EXTERN(30) FBF_EXTERN(31)
-FBF_EXTERN(32)
-#undef FBF_EXTERN
-#undef FBF_EXTERN1
+#include "fbf_kernel_extern.inc"
 
 namespace {
 
 using LaunchFn = cudaError_t (*)(const Params&, int, cudaStream_t);
-struct RadiusEntry {
-    LaunchFn launch[kMaxKR + 1];  // by NKR (number of k >= 1 terms in the launch)
-    int max_pairs[3];             // by CTAs per SM (index 1, 2)
-    int fsw;                      // TMA box width
-    size_t pair_bytes, fixed_bytes;
+// One step-height variant of a radius: launchers by NKR (number of k >= 1 terms
+// in the launch) and the channel pairs that fit per CTA for each (gen buffers,
+// column buffers) choice.
+struct QEntry {
+    LaunchFn launch[kMaxKR + 1] = {};
+    int max_pairs[3][3] = {};  // [ngb][ncb], 1..2
 };
+struct RadiusEntry {
+    QEntry split8;          // split mode, Q = 8 (every radius)
+    QEntry pair8, pair16;   // pair mode, r <= kQ16MaxRadius
+};
+
+template <int R, int Q, int M>
+QEntry qentry() {
+    using G = Geometry<R, Q, M>;
+    QEntry e;
+    e.launch[0] = &launch_fused<R, Q, 0, M>;
+    e.launch[1] = &launch_fused<R, Q, 1, M>;
+    e.launch[2] = &launch_fused<R, Q, 2, M>;
+    e.launch[3] = &launch_fused<R, Q, 3, M>;
+    e.launch[4] = &launch_fused<R, Q, 4, M>;
+    for (int ngb = 1; ngb <= 2; ++ngb)
+        for (int ncb = 1; ncb <= 2; ++ncb) e.max_pairs[ngb][ncb] = G::max_pairs(ngb, ncb);
+    return e;
+}
 
 template <int R>
 RadiusEntry entry() {
-    using G = Geometry<R>;
-    return {{&launch_fused<R, 0>, &launch_fused<R, 1>, &launch_fused<R, 2>, &launch_fused<R, 3>,
-             &launch_fused<R, 4>},
-            {0, G::max_pairs(1), G::max_pairs(2)},
-            G::FSW,
-            G::pair_bytes,
-            G::fixed_bytes};
+    RadiusEntry e;
+#ifdef FBF_DEV_RADIUS  // dev builds with a single radius specialised (build.py --radius)
+    if constexpr (R != FBF_DEV_RADIUS) return e;
+#endif
+    e.split8 = qentry<R, 8, kSplitMode>();
+    if constexpr (R <= kQ16MaxRadius) {
+        e.pair8 = qentry<R, 8, kPairMode>();
+        e.pair16 = qentry<R, 16, kPairMode>();
+    }
+    return e;
 }
 
 const RadiusEntry& radius_entry(int r) {
@@ -201,7 +212,8 @@ struct Chunk {
 
 struct Plan {
     std::vector<Chunk> chunks;
-    int blocks_per_sm = 1;
+    int q = 8, mode = 1, ngb = 2, ncb = 2;
+    const fbf_dev::QEntry* ent = nullptr;
 };
 
 // Split k = 0..K-1 into launches whose channel pairs fit in shared memory
@@ -230,11 +242,63 @@ std::vector<Chunk> split_chunks(int K, int max_pairs) {
     return out;
 }
 
-// One CTA per SM (the three warp roles already overlap latency-bound and
-// FFMA2-bound phases; registers allow no second CTA).
+int env_int(const char* name) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : 0;
+}
+
+// FFMA2 warps per SM sub-partition (warp id mod 4) are what limits a CTA:
+// the busiest sub-partition sets the pace, so a layout with w FFMA2 warps of
+// equal work reaches at most w / (4 ceil(w / 4)) of the FMA peak.
+double subpartition_balance(int warps) { return warps / (4.0 * ((warps + 3) / 4)); }
+
+// One CTA per SM. Variant choice: fewest coefficient chunks first, then the
+// best sub-partition balance of the FFMA2 warps (pair mode: one warp per
+// channel pair; split mode: two), then the first entry of the measured
+// preference list (step height Q, mode, gen buffers, column buffers).
+// FBF_Q, FBF_MODE, FBF_NGB, FBF_NCB override (tuning).
 Plan make_plan(int K, int r) {
     const auto& ent = fbf_dev::radius_entry(r);
-    return Plan{split_chunks(K, ent.max_pairs[1]), 1};
+    static const int fq = env_int("FBF_Q"), fngb = env_int("FBF_NGB"), fncb = env_int("FBF_NCB");
+    static const int fmode = std::getenv("FBF_MODE") ? env_int("FBF_MODE") : -1;
+    struct Pref {
+        int q, mode, ngb, ncb;
+    };
+    constexpr int P = fbf_dev::kPairMode, S = fbf_dev::kSplitMode;
+    static const Pref prefs[] = {{16, P, 2, 2}, {8, P, 2, 2}, {8, S, 2, 2}, {16, P, 2, 1},
+                                 {8, P, 1, 1}, {8, S, 1, 1}, {16, P, 1, 1}};
+    Plan best;
+    double best_bal = -1.0;
+    for (const Pref& pf : prefs) {
+        const fbf_dev::QEntry* qe = pf.mode == S ? &ent.split8 : pf.q == 16 ? &ent.pair16 : &ent.pair8;
+        if (!qe->launch[0] || (fq && fq != pf.q) || (fmode >= 0 && fmode != pf.mode) || (fngb && fngb != pf.ngb) ||
+            (fncb && fncb != pf.ncb))
+            continue;
+        const int mp = qe->max_pairs[pf.ngb][pf.ncb];
+        if (mp < 2) continue;
+        auto chunks = split_chunks(K, mp);
+        double bal = 1.0;
+        for (const Chunk& c : chunks)
+            bal = std::min(bal, subpartition_balance((pf.mode == S ? 2 : 1) * c.n_pairs));
+        const bool better = best_bal < 0 || chunks.size() < best.chunks.size() ||
+                            (chunks.size() == best.chunks.size() && bal > best_bal + 1e-9);
+        if (better) {
+            best = Plan{std::move(chunks), pf.q, pf.mode, pf.ngb, pf.ncb, qe};
+            best_bal = bal;
+        }
+    }
+    return best;
+}
+
+// dev builds (FBF_PHASES) with FBF_PROF=1: per-warp-slot cycle counters
+unsigned long long* g_prof = nullptr;
+unsigned long long* dev_prof_buffer() {
+#ifdef FBF_PHASES
+    static const bool on = std::getenv("FBF_PROF") != nullptr;
+    if (on && !g_prof && cudaMalloc(&g_prof, 128 * sizeof(unsigned long long)) == cudaSuccess)
+        cudaMemset(g_prof, 0, 128 * sizeof(unsigned long long));
+#endif
+    return g_prof;
 }
 
 struct Job {
@@ -253,8 +317,8 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
             float2* scratch, unsigned long long* d_fallbacks, cudaStream_t stream,
             unsigned int* d_bad = nullptr) {
     const int r = (int)std::ceil(3.0 * theta);
-    const auto& ent = fbf_dev::radius_entry(r);
     const Plan plan = make_plan(a.K, r);
+    if (!plan.ent) return fail(FBF_ECAPACITY, "no kernel variant fits the shared memory for this radius");
     if (plan.chunks.size() > 1 && !scratch) return fail(FBF_EINVAL, "internal: scratch required");
 
     fbf_dev::Params p{};
@@ -281,7 +345,7 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
     p.total_units = (long long)job.n_frames * p.n_strips * job.out_rows;
     // kernels.cpp:105-118 taps, kept by |d|
     for (int j = 0; j <= r; ++j)
-        p.taps[j] = (float)std::exp(-((double)j * j) / (2.0 * theta * theta));
+        p.taps[j] = p.taps_col[j] = (float)std::exp(-((double)j * j) / (2.0 * theta * theta));
     // interior row spans go through the TMA bulk-copy engine when rows are 16-byte aligned
     // Interior f rows: element cp.async by default (measured fastest on B200:
     // profiles/r01_stage_modes.txt); FBF_STAGE=bulk routes them through the TMA
@@ -293,10 +357,14 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
     const bool aligned = job.width % 4 == 0 && ((uintptr_t)job.d_src & 15) == 0 &&
                          (job.n_frames == 1 || job.src_frame_stride % 4 == 0);
     p.use_tma = aligned ? stage_mode : 0;
+    p.vec_ok = aligned ? 1 : 0;
     // persistent grid: CTAs per SM x SMs, but keep segments at least a few steps long
-    const long long min_seg = 4 * fbf_dev::kQ;
+    p.ngb = plan.ngb;
+    p.prof = dev_prof_buffer();
+    p.ncb = plan.ncb;
+    const long long min_seg = 4 * plan.q;
     const long long want = (p.total_units + min_seg - 1) / min_seg;
-    const int grid = (int)std::max(1LL, std::min<long long>((long long)ctx.num_sms * plan.blocks_per_sm, want));
+    const int grid = (int)std::max(1LL, std::min<long long>((long long)ctx.num_sms, want));
 
     for (size_t ci = 0; ci < plan.chunks.size(); ++ci) {
         const Chunk& c = plan.chunks[ci];
@@ -309,7 +377,7 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
         for (int kk = 0; kk < c.n_k; ++kk) p.coeff[kk] = (float)a.c[c.k_lo + kk];
         p.inv_period = (float)(1.0 / (2.0 * a.T + 1.0));
         p.k_first = std::max(c.k_lo, 1);
-        const cudaError_t e = ent.launch[nkr](p, grid, stream);
+        const cudaError_t e = plan.ent->launch[nkr](p, grid, stream);
         if (e != cudaSuccess) return cuda_fail(e, "fbf_fused_kernel launch");
         g_launches.fetch_add(1, std::memory_order_relaxed);
     }
@@ -474,6 +542,15 @@ int fbf_set_device(int device) {
 int fbf_get_device(void) { return g_default_device.load(); }
 
 unsigned long long fbf_kernel_launches(void) { return g_launches.load(); }
+
+// dev: read and reset the FBF_PHASES per-warp-slot counters (128 values); -1 if absent
+int fbf_dev_prof(unsigned long long* out) {
+    if (!fbf_b200::g_prof) return -1;
+    cudaDeviceSynchronize();
+    cudaMemcpy(out, fbf_b200::g_prof, 128 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaMemset(fbf_b200::g_prof, 0, 128 * sizeof(unsigned long long));
+    return 0;
+}
 
 int fbf_device_count(void) {
     int n = 0;

@@ -9,32 +9,33 @@
 //   combine + fallback                    (src/filter.cpp:197-211)
 // without materialising any of the 4K-2 auxiliary images in HBM.
 //
-// Dataflow (persistent CTAs, column strips streamed top to bottom, two
-// warp-specialised roles connected by mbarriers so that the latency-bound
-// phases of one overlap the FFMA2-bound phases of the other):
+// Dataflow (persistent CTAs, column strips streamed top to bottom, warp roles
+// connected by mbarriers):
 //   * The image is cut into strips of TW=32 output columns. Each CTA owns a
 //     contiguous range of (frame, strip, row) units -- one or a few strip
 //     segments -- so every CTA gets the same number of output rows.
-//   * A segment is streamed in steps of Q=8 input rows. Producer warps run
-//     stage + gen + row for step s while consumer warps run col + comb for
-//     step s-1; ring blocks are handed over with full/empty mbarriers.
-//       stage: a loader warp fetches f tiles (Q rows x (TW+2r) columns) up to
-//              three steps ahead: one TMA bulk copy per row (cp.async.bulk,
-//              mbarrier complete_tx) for interior tiles, border-mapped
-//              element loads at the image edges (the copy engine cannot mirror).
-//       gen  : channel pairs (f, 1) for k = 0 and (C_k f, S_k f), (C_k, S_k)
-//              for k >= 1, with C_k + i S_k = exp(i k nu f) from one
-//              double-reduced MUFU sincos and the angle-addition recurrence.
-//       row  : horizontal (2r+1)-tap pass of every channel pair, 8 outputs
-//              per thread, FFMA2 with the tap broadcast from a uniform
-//              register; results go to a ring of 1 + ceil(2r/Q) row blocks.
-//       col  : vertical pass over the ring, 8 outputs per thread, FFMA2; the
-//              ring window resolves to fixed offsets at compile time.
-//       comb : per output pixel, num += c_k (C_k G(C_k f) + S_k G(S_k f)),
+//   * A segment is streamed in steps of Q input rows (Q = 16 for radii <= 16,
+//     else 8; every FFMA2 lane produces P = Q outputs per pass).
+//       LOAD : one warp stages f tiles (Q rows x (TW+2r) columns, border-mapped
+//              through precomputed column maps) with 4-byte cp.async, up to two
+//              steps ahead.
+//       GEN  : channel pairs (f, 1) for k = 0 and (C_k f, S_k f), (C_k, S_k)
+//              for k >= 1, with C_k + i S_k = exp(i k nu f) from one MUFU
+//              sincos and the angle-addition recurrence, two pixels per thread
+//              in packed FP32.
+//       ROW  : one warp per channel pair: horizontal (2r+1)-tap pass, FFMA2
+//              with the tap broadcast from a uniform register, into the pair's
+//              ring of 1 + ceil(2r/Q) + 1 row blocks.
+//       COL  : one warp per channel pair: vertical pass over the ring (window
+//              offsets resolve at compile time) into a column-result tile.
+//       COMB : num += c_k (C_k G(C_k f) + S_k G(S_k f)),
 //              den += c_k (C_k G(C_k) + S_k G(S_k)) in ascending k, then
-//              out = den > 1e-12 ? num / den : f.
+//              out = den > 1e-12 ? num / den : f; fallback count; the range
+//              check of filter.cpp:19-23 on every output pixel's f.
 //   * Channel pairs share taps, so one FFMA2 advances two channels (the
-//     reference's 4K-2 channels are exactly 2K-1 pairs).
+//     reference's 4K-2 channels are exactly 2K-1 pairs). Row and column passes
+//     of a pair run in different warps so that the 2(2K-1) FFMA2 warps spread
+//     evenly over the four SM sub-partitions (warp id mod 4).
 //   * Coefficient chunks: when 2K-1 pairs do not fit in shared memory the
 //     host launches one pass per chunk of k; (num, den) are carried in a
 //     float2 scratch image between passes, still in ascending k.
@@ -43,45 +44,38 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace fbf_dev {
 
 constexpr int kTW = 32;          // output columns per strip
-#ifndef FBF_Q
-#define FBF_Q 8
-#endif
-constexpr int kQ = FBF_Q;        // input rows per pipeline step
-constexpr int kP = 8;            // outputs per thread item (row and column passes)
 constexpr int kMaxKR = 4;        // k >= 1 terms per launch (template parameter NKR <= kMaxKR)
 constexpr int kMaxPairs = 1 + 2 * kMaxKR;
 constexpr int kMaxRadius = 32;
-constexpr int kItemsPerPair = kQ * kTW / kP;  // 32 threads (one warp) per channel pair and role
-constexpr int kRoles = 2;        // pair warps and gen warps scale with the pairs
-constexpr int kCombThreads = kQ * kTW / 2;  // combine warps: one pixel pair per thread
-constexpr int kExtraThreads = kCombThreads + 32;  // + combine + loader
-constexpr int kMaxThreads = kRoles * kMaxPairs * kItemsPerPair + kExtraThreads;
+constexpr int kQ16MaxRadius = 16;  // Q = 16 steps are instantiated for r <= 16
+constexpr int kCombWarps = 4;
+constexpr int kCombThreads = kCombWarps * 32;
+constexpr int kGenWarps = 4;
+constexpr int kGenThreads = kGenWarps * 32;
+constexpr int kExtraThreads = kCombThreads + kGenThreads + 32;  // combine + gen + loader
 constexpr size_t kSmemLimit = 232448;          // 227 KB opt-in per block on sm_100
 constexpr size_t kSmemPerSM = 233472;          // 228 KB per SM
 constexpr size_t kSmemReservedPerBlock = 1024;
 
-static_assert(kQ % kP == 0, "column-pass row groups tile the step");
+// Warp organisations of the FFMA2 work (template parameter M):
+//   kPairMode : one warp per channel pair runs the row pass AND the (scatter)
+//               column pass of a step -- no cross-warp handoff between passes
+//               (r <= 16, where the 2r column partial sums fit in registers);
+//   kSplitMode: one ROW and one COL warp per pair, connected by a ring of row
+//               blocks -- twice the warps, so the FFMA2 work spreads more evenly
+//               over the four SM sub-partitions (warp id mod 4).
+constexpr int kPairMode = 0, kSplitMode = 1;
+// threads of a launch: FFMA2 warps, plus combine, gen and loader
+__host__ __device__ constexpr int block_threads(int pairs, int mode) {
+    return (mode == kPairMode ? 1 : 2) * 32 * pairs + kExtraThreads;
+}
+enum Role { kRoleGen = 0, kRoleRow = 1, kRoleCol = 2, kRoleLoad = 3, kRoleComb = 4, kRoleIdle = 5 };
 
-#ifdef FBF_PHASES
-// dev instrumentation: per-role cycle counters (thread 0 of each role)
-__device__ unsigned long long g_phase_cycles[16];
-__device__ unsigned long long g_cta_cycles[1024];
-#define FBF_PHASE_T0() long long _ph_t = clock64()
-#define FBF_PHASE(i)                                                        \
-    do {                                                                    \
-        if (tid == 0) {                                                     \
-            long long _n = clock64();                                       \
-            atomicAdd(&g_phase_cycles[i], (unsigned long long)(_n - _ph_t)); \
-            _ph_t = _n;                                                     \
-        }                                                                   \
-    } while (0)
-#else
-#define FBF_PHASE_T0()
-#define FBF_PHASE(i)
-#endif
 
 struct Params {
     const float* src;            // frame 0, global row src_row0, column 0
@@ -103,38 +97,74 @@ struct Params {
     int first_chunk, last_chunk;
     int n_strips;
     int use_tma;                 // interior f tiles through the TMA bulk-copy engine
+    int vec_ok;                  // rows are 16-byte aligned: interior tiles with 16-byte cp.async
+    int ngb, ncb;                // gen / column-result buffers (1..2 each)
     long long total_units;       // n_frames * n_strips * out_rows
-    float taps[kMaxRadius + 1];  // taps[j] = exp(-j^2 / (2 theta^2)), j = |d|
+    float taps[kMaxRadius + 1];  // taps[j] = exp(-j^2 / (2 theta^2)), j = |d| (row pass)
+    // the same taps for the column pass: a second copy keeps ptxas from hoisting
+    // the shared values into ordinary registers when one warp runs both passes;
+    // as separate kernel-parameter values each pass takes them as uniform-register
+    // FFMA2 operands (measured: register operands cost FFMA2 issue rate)
+    float taps_col[kMaxRadius + 1];
     float coeff[kMaxKR + 1];     // c_k of the chunk, ascending k
     float inv_period;            // 1 / (2T + 1)
+    unsigned long long* prof;    // dev builds with FBF_PHASES: per warp slot [total, wait A, wait B, CTAs] cycles
 };
 
-template <int R>
+#ifdef FBF_PHASES
+#define PWAIT(k, bar, par)                      \
+    do {                                        \
+        const long long _t0 = clock64();        \
+        mbar_wait(bar, par);                    \
+        _pw[k] += clock64() - _t0;              \
+    } while (0)
+#define PSYNC(k, id, n)                         \
+    do {                                        \
+        const long long _t0 = clock64();        \
+        named_sync(id, n);                      \
+        _pw[k] += clock64() - _t0;              \
+    } while (0)
+#else
+#define PWAIT(k, bar, par) mbar_wait(bar, par)
+#define PSYNC(k, id, n) named_sync(id, n)
+#endif
+
+template <int R, int Q, int M>
 struct Geometry {
+    static_assert(Q == 8 || Q == 16, "step height");
+    static constexpr bool PAIR = M == kPairMode;
     static constexpr int GW = kTW + 2 * R;                       // gen row width (pixels)
     static constexpr int GS = GW + ((2 - GW % 4) + 4) % 4;       // gen stride (float2), GS/2 odd
     static constexpr int FSW = (GW + 3 + 3) / 4 * 4;             // f staging row: GW + 16B-alignment slack
-    static constexpr int RB = 1 + (2 * R + kQ - 1) / kQ;         // ring blocks a column pass reads
-    static constexpr int RBP = RB + 1;                           // + the block the next row pass writes
-    static constexpr int RROWS = RBP * kQ;                       // ring rows (private to a pair warp)
+    // Column pass form: for R <= kScatterMaxRadius the 2R partial sums of a column
+    // live in registers ("scatter": every row-pass output is read once), so the
+    // ring is just a double buffer of Q rows; larger radii gather a window of
+    // ring rows (RB blocks) per step.
+    static constexpr bool SCATTER = R <= 16;
+    static_assert(SCATTER || !PAIR, "pair mode keeps the column partial sums in registers");
+    static constexpr int RB = 1 + (2 * R + Q - 1) / Q;           // ring blocks a gather column pass reads
+    static constexpr int RBN = SCATTER ? 1 : RB;                 // blocks a column pass reads
+    // + the block the next row pass writes (split mode); pair mode: the warp's own
+    // row pass of the next step starts after its column pass, one block suffices
+    static constexpr int RBP = PAIR ? 1 : RBN + 1;
+    static constexpr int RROWS = RBP * Q;                        // ring rows per pair
     static constexpr int RS = kTW + 2;                           // ring stride (float2), RS/2 odd
     static constexpr int NFS = 3;                                // f staging buffers (loader runs ahead)
-#ifndef FBF_NGB
-#define FBF_NGB 2
-#endif
-    static constexpr int NGB = FBF_NGB;                          // gen buffers (gen runs ahead)
-    static constexpr int NCB = 2;                                // column-result buffers
-    static constexpr size_t fstage_bytes = sizeof(float) * NFS * kQ * FSW;  // multiple of 128
-    static constexpr size_t bar_bytes = 8 * (2 * NFS + 2 * NGB + 2 * NCB) + 8;  // mbarriers + counter
+    static constexpr int kMaxBuf = 2;                            // gen / column buffers (named barrier ids)
+    static constexpr size_t fstage_bytes = sizeof(float) * NFS * Q * FSW;  // multiple of 128
+    static constexpr int n_bars = NFS + 2 * kMaxPairs * RBP;
+    static constexpr size_t bar_bytes = 8 * n_bars + 8;          // mbarriers + counter
     static constexpr size_t misc_bytes = (bar_bytes + 127) / 128 * 128;
     static constexpr size_t fixed_bytes = fstage_bytes + misc_bytes;
-    static constexpr size_t pair_bytes = sizeof(float2) * (size_t)(NGB * kQ * GS + NCB * kQ * kTW + RROWS * RS);
-    static constexpr size_t smem_bytes(int pairs) { return fixed_bytes + pair_bytes * pairs; }
-    static int max_pairs(int blocks_per_sm) {
-        size_t budget = kSmemPerSM / blocks_per_sm - kSmemReservedPerBlock;
+    static constexpr size_t pair_bytes(int ngb, int ncb) {
+        return sizeof(float2) * (size_t)(ngb * Q * GS + ncb * Q * kTW + RROWS * RS);
+    }
+    static constexpr size_t smem_bytes(int pairs, int ngb, int ncb) { return fixed_bytes + pair_bytes(ngb, ncb) * pairs; }
+    static int max_pairs(int ngb, int ncb) {
+        size_t budget = kSmemPerSM - kSmemReservedPerBlock;
         if (budget > kSmemLimit) budget = kSmemLimit;
         if (budget <= fixed_bytes) return 0;
-        const size_t p = (budget - fixed_bytes) / pair_bytes;
+        const size_t p = (budget - fixed_bytes) / pair_bytes(ngb, ncb);
         return (int)(p < (size_t)kMaxPairs ? p : (size_t)kMaxPairs);
     }
 };
@@ -150,46 +180,15 @@ __host__ __device__ __forceinline__ int map_border(int i, int n, int border) {
     return m < n ? m : period - 1 - m;
 }
 
-// (cos, sin)(2 pi f / (2T+1)): turn reduction (exact: |t| < 1), then the MUFU
-// pair on [-pi, pi].
-__device__ __forceinline__ float2 harmonic1(float f, float inv_period) {
-    float t = f * inv_period;
-    t -= rintf(t);
-    float s, c;
-    __sincosf(t * 6.28318530717958647692f, &s, &c);
-    return make_float2(c, s);
-}
-
-// exp(i (k+1) w) = exp(i k w) * exp(i w). gen and combine run this identical
-// sequence, so modulation and demodulation factors agree bit for bit and do not
-// depend on how k is split into chunks.
-__device__ __forceinline__ float2 rotate(float2 cs, float2 c1) {
-    return make_float2(fmaf(cs.x, c1.x, -(cs.y * c1.y)), fmaf(cs.y, c1.x, cs.x * c1.y));
-}
-
-// Complex rotation z * w with packed FP32: t = z.x (w.x, w.y); z' = z.y (-w.y, w.x) + t,
-// u = (-w.y, w.x) precomputed. gen and combine share this exact sequence.
-__device__ __forceinline__ float2 cmul_rot(float2 z, float2 w, float2 u) {
-    return __ffma2_rn(make_float2(z.y, z.y), u, __fmul2_rn(make_float2(z.x, z.x), w));
-}
-__device__ __forceinline__ float2 harmonic1c(float f, float inv_period) {
-    float t = f * inv_period;
-    t -= rintf(t);
-    float sn, cs;
-    __sincosf(t * 6.28318530717958647692f, &sn, &cs);
-    return make_float2(cs, sn);
-}
-__device__ __forceinline__ float2 harmonic_firstc(float2 w, float2 u, int k_first) {
-    float2 z = w;
-    for (int k = 1; k < k_first; ++k) z = cmul_rot(z, w, u);
-    return z;
-}
-
-// Packed forms for two adjacent pixels: (C, S) hold the two pixels' cosines and
-// sines, per-lane arithmetic identical to rotate() / harmonic1().
+// Packed forms for two adjacent pixels: (c, s) hold the two pixels' cosines and
+// sines. exp(i (k+1) w) = exp(i k w) * exp(i w); gen and combine run this
+// identical sequence, so modulation and demodulation factors agree bit for bit
+// and do not depend on how k is split into chunks.
 struct CS2 {
     float2 c, s;
 };
+// (cos, sin)(2 pi f / (2T+1)): turn reduction (exact: |t| < 1), then the MUFU
+// pair on [-pi, pi].
 __device__ __forceinline__ CS2 harmonic1x2(float2 f, float inv_period) {
     float2 t = __fmul2_rn(f, make_float2(inv_period, inv_period));
     t = make_float2(t.x - rintf(t.x), t.y - rintf(t.y));
@@ -199,23 +198,28 @@ __device__ __forceinline__ CS2 harmonic1x2(float2 f, float inv_period) {
     __sincosf(t.y, &r.s.y, &r.c.y);
     return r;
 }
-__device__ __forceinline__ CS2 rotate2(CS2 v, CS2 w, float2 nws) {  // nws = -w.s
+// One rotation step, per component: C' = fma(-S, s, C c), S' = fma(C, s, S c).
+// rotate2 works on two pixels packed per component, rotate1 on one pixel packed
+// as (C, S) (one FMUL2 + one FFMA2 with a swapped, half-negated operand); both
+// round identically, so gen (rotate1) and combine (rotate2) agree bit for bit.
+__device__ __forceinline__ CS2 rotate2(CS2 v, CS2 w) {
     CS2 r;
-    r.c = __ffma2_rn(v.c, w.c, __fmul2_rn(v.s, nws));
-    r.s = __ffma2_rn(v.s, w.c, __fmul2_rn(v.c, w.s));
+    r.c = __ffma2_rn(make_float2(-v.s.x, -v.s.y), w.s, __fmul2_rn(v.c, w.c));
+    r.s = __ffma2_rn(v.c, w.s, __fmul2_rn(v.s, w.c));
     return r;
 }
+__device__ __forceinline__ float2 rotate1(float2 z, float2 w) {
+    return __ffma2_rn(make_float2(-z.y, z.x), make_float2(w.y, w.y), __fmul2_rn(z, make_float2(w.x, w.x)));
+}
 __device__ __forceinline__ CS2 harmonic_first2(CS2 c1, int k_first) {
-    const float2 nws = make_float2(-c1.s.x, -c1.s.y);
     CS2 cs = c1;
-    for (int k = 1; k < k_first; ++k) cs = rotate2(cs, c1, nws);
+    for (int k = 1; k < k_first; ++k) cs = rotate2(cs, c1);
     return cs;
 }
-
-__device__ __forceinline__ float2 harmonic_first(float2 c1, int k_first) {
-    float2 cs = c1;
-    for (int k = 1; k < k_first; ++k) cs = rotate(cs, c1);
-    return cs;
+__device__ __forceinline__ float2 harmonic_first1(float2 w, int k_first) {
+    float2 z = w;
+    for (int k = 1; k < k_first; ++k) z = rotate1(z, w);
+    return z;
 }
 
 __device__ __forceinline__ float2 ffma2(float2 a, float w, float2 c) {
@@ -225,9 +229,6 @@ __device__ __forceinline__ float2 ffma2(float2 a, float w, float2 c) {
 // ---- synchronisation / async copy primitives -------------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void named_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc));
@@ -240,17 +241,11 @@ __device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
 }
 // raise the expected transaction bytes of the current phase (no arrival)
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
@@ -271,9 +266,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "r"(parity), "r"(1000000u)
         : "memory");
 }
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+// Named CTA barriers for the warp-role handoffs: producers bar.arrive (no
+// wait), consumers bar.sync -- a consumer warp blocked in bar.sync issues
+// nothing, where an mbarrier try_wait loop keeps waking up (measured: the
+// polling of idle gen/combine/loader warps cost about a third of all issued
+// instructions). bar.arrive / bar.sync order shared-memory accesses among the
+// participating threads.
+__device__ __forceinline__ void named_arrive(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+// barrier ids (0 is __syncthreads): gen full/empty, column full/empty, f stage empty
+constexpr int kBarGenFull = 1, kBarGenEmpty = 3, kBarColFull = 5, kBarColEmpty = 7, kBarFsEmpty = 9;
+
 // 1-D TMA bulk copy global -> shared (16-byte aligned, size multiple of 16),
 // completion on `bar`.
 __device__ __forceinline__ void tma_bulk_g2s(float* smem_dst, const float* gsrc, unsigned bytes, uint64_t* bar) {
@@ -283,193 +290,161 @@ __device__ __forceinline__ void tma_bulk_g2s(float* smem_dst, const float* gsrc,
                  : "memory");
 }
 
-// Vertical pass for output rows [Q0, Q0 + kP) of global step g. The window
-// rows j in [Q0 - 2R, Q0 + kP) (relative to block g) resolve to (block, row)
-// at compile time, so every load is a fixed offset from one of RB block pointers.
-template <int R, int Q0>
-__device__ __forceinline__ void column_pass(const float2* __restrict__ ring_pair, int blk, int x,
-                                            const float* taps, float* out_col) {
-    using G = Geometry<R>;
-    constexpr int RB = G::RB, RS = G::RS;
-    const float2* bptr[RB];
+// Horizontal pass of one step for one channel pair: lane = (row q, chunk of Q
+// columns); Q outputs per lane from (Q+2R)/2 LDS.128 of gen row q. Arrives on
+// `gen_empty` once the gen rows are read, then writes the ring block.
+template <int R, int Q>
+__device__ __forceinline__ void row_pass(const float4* __restrict__ gin, float4* __restrict__ hout, const Params& pp,
+                                         int gen_empty_id, int gen_threads) {
+    float2 acc[Q];
 #pragma unroll
-    for (int b = 0; b < RB; ++b) {  // bptr[b] = block (blk - b) mod RB
-        int bb = blk - b;
-        bb += bb < 0 ? RB : 0;
-        bptr[b] = ring_pair + bb * kQ * RS + x;
-    }
-    float2 acc[kP];
+    for (int o = 0; o < Q; ++o) acc[o] = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int o = 0; o < kP; ++o) acc[o] = make_float2(0.f, 0.f);
+    for (int j = 0; j < (Q + 2 * R) / 2; ++j) {
+        const float4 v4 = gin[j];
 #pragma unroll
-    for (int i = 0; i < kP + 2 * R; ++i) {
-        const int j = Q0 + i - 2 * R;                     // compile-time
-        const int b = j >= 0 ? 0 : (-j + kQ - 1) / kQ;    // blocks back
-        const float2 v = bptr[b][(j + b * kQ) * RS];
+        for (int h = 0; h < 2; ++h) {
+            const int jj = 2 * j + h;
+            const float2 v = h ? make_float2(v4.z, v4.w) : make_float2(v4.x, v4.y);
 #pragma unroll
-        for (int o = 0; o < kP; ++o) {
-            const int d = i - o;
-            if (d >= 0 && d <= 2 * R) acc[o] = ffma2(v, taps[d >= R ? d - R : R - d], acc[o]);
+            for (int o = 0; o < Q; ++o) {
+                const int d = jj - o;  // tap index 0..2R, ascending per output
+                if (d >= 0 && d <= 2 * R) acc[o] = ffma2(v, pp.taps[d >= R ? d - R : R - d], acc[o]);
+            }
         }
     }
+    named_arrive(gen_empty_id, gen_threads);  // this warp's gen rows consumed
 #pragma unroll
-    for (int o = 0; o < kP; ++o) {  // planar: [q][component][TW]
-        float* oc = out_col + (Q0 + o) * 2 * kTW;
-        oc[0] = acc[o].x;
-        oc[kTW] = acc[o].y;
-    }
+    for (int o = 0; o < Q / 2; ++o)
+        hout[o] = make_float4(acc[2 * o].x, acc[2 * o].y, acc[2 * o + 1].x, acc[2 * o + 1].y);
 }
 
-// One software-pipelined pair-warp iteration: the horizontal pass of step t
-// (DO_ROW; lane = (row q, 8-column chunk)) interleaved with the vertical pass of
-// step t-1 (DO_COL; lane = column). The two FFMA2 streams are independent, so each
-// hides the other's shared-memory latency. Row loads: (8+2R)/2 float4, column
-// loads: 8+2R float2 -- always 2 column rows per row chunk.
-template <int R, bool DO_ROW, bool DO_COL>
-__device__ __forceinline__ void pair_iter(const float4* __restrict__ gin, float2* ring_pair, int blk_row,
-                                          int blk_col, int lane, const float* taps, float* out_col,
-                                          uint64_t* gen_empty_bar) {
-    using G = Geometry<R>;
+// Vertical pass of ring block `blk` (the step's Q rows): lane = column, Q
+// outputs from Q+2R ring rows. Window row jr (relative to the block's first row)
+// resolves to (block, row) at compile time, so every load is a fixed offset
+// from one of RB block pointers.
+template <int R, int Q>
+__device__ __forceinline__ void col_pass(const float2* __restrict__ ring_pair, int blk, int lane, const Params& pp,
+                                         float2 (&acc)[Q]) {
+    using G = Geometry<R, Q, kSplitMode>;
     constexpr int RB = G::RB, RBP = G::RBP, RS = G::RS;
-    const int q = lane % kQ, xc = lane / kQ;
-    float2 accr[kP], accc[kP];
     const float2* bptr[RB];
 #pragma unroll
-    for (int o = 0; o < kP; ++o) {
-        accr[o] = make_float2(0.f, 0.f);
-        accc[o] = make_float2(0.f, 0.f);
-    }
-    if (DO_COL) {
-#pragma unroll
-        for (int b = 0; b < RB; ++b) {  // bptr[b] = block (blk_col - b) mod RBP
-            int bb = blk_col - b;
-            bb += bb < 0 ? RBP : 0;
-            bptr[b] = ring_pair + bb * kQ * RS + lane;
-        }
+    for (int b = 0; b < RB; ++b) {  // bptr[b] = block (blk - b) mod RBP
+        int bb = blk - b;
+        bb += bb < 0 ? RBP : 0;
+        bptr[b] = ring_pair + bb * Q * RS + lane;
     }
 #pragma unroll
-    for (int j = 0; j < (kP + 2 * R) / 2; ++j) {
-        if (DO_ROW) {
-            const float4 v4 = gin[j];
+    for (int o = 0; o < Q; ++o) acc[o] = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int jj = 2 * j + h;
-                const float2 v = h ? make_float2(v4.z, v4.w) : make_float2(v4.x, v4.y);
+    for (int i = 0; i < Q + 2 * R; ++i) {
+        const int jr = i - 2 * R;                        // window row, compile-time
+        const int b = jr >= 0 ? 0 : (-jr + Q - 1) / Q;   // blocks back
+        const float2 v = bptr[b][(jr + b * Q) * RS];
 #pragma unroll
-                for (int o = 0; o < kP; ++o) {
-                    const int d = jj - o;  // tap index 0..2R, ascending per output
-                    if (d >= 0 && d <= 2 * R) accr[o] = ffma2(v, taps[d >= R ? d - R : R - d], accr[o]);
-                }
-            }
-        }
-        if (DO_COL) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int i = 2 * j + h;
-                const int jr = i - 2 * R;                       // window row, compile-time
-                const int b = jr >= 0 ? 0 : (-jr + kQ - 1) / kQ;  // blocks back
-                const float2 v = bptr[b][(jr + b * kQ) * RS];
-#pragma unroll
-                for (int o = 0; o < kP; ++o) {
-                    const int d = i - o;
-                    if (d >= 0 && d <= 2 * R) accc[o] = ffma2(v, taps[d >= R ? d - R : R - d], accc[o]);
-                }
-            }
-        }
-    }
-    if (DO_ROW) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(gen_empty_bar);  // this warp's gen rows consumed
-        float4* hout = reinterpret_cast<float4*>(ring_pair + ((size_t)blk_row * kQ + q) * RS + xc * kP);
-#pragma unroll
-        for (int o = 0; o < kP / 2; ++o)
-            hout[o] = make_float4(accr[2 * o].x, accr[2 * o].y, accr[2 * o + 1].x, accr[2 * o + 1].y);
-    }
-    if (DO_COL) {
-#pragma unroll
-        for (int o = 0; o < kP; ++o) {  // planar: [q][component][TW]
-            float* oc = out_col + o * 2 * kTW + lane;
-            oc[0] = accc[o].x;
-            oc[kTW] = accc[o].y;
+        for (int o = 0; o < Q; ++o) {
+            const int d = i - o;
+            if (d >= 0 && d <= 2 * R) acc[o] = ffma2(v, pp.taps_col[d >= R ? d - R : R - d], acc[o]);
         }
     }
 }
 
-// Warp roles (np = channel pairs of the launch):
-//   PAIR (np warps) : warp p owns channel pair p: horizontal pass of the step's
-//                     Q rows into ITS OWN ring, then the vertical pass of the step
-//                     from that ring into a column buffer -- no cross-warp handoff
-//                     between the two passes
-//   GEN  (np warps) : channel pairs of the next step into one of 2 gen buffers
-//   COMB (4 warps)  : combine + divide, one output pixel pair per thread
-//   LOAD (1 warp)   : f tiles into one of 3 staging buffers
-// Handoffs GEN -> PAIR -> COMB and LOAD -> GEN are full/empty mbarrier pairs
-// with per-warp arrivals, so no role waits for a sibling warp.
+// Scatter form of the vertical pass for the Q rows of one ring block (lane =
+// column). st[i] holds the partial sum of output row y - R + 1 + i after input
+// row y; each new row v adds w(|d|) v to the 2R pending outputs while shifting
+// them down one slot (one FFMA2 each, in place in ascending i), and completes
+// output row y - R. Contributions enter every output in ascending input row,
+// the reference's order (filter.cpp:52-70), so the result is bit-identical to
+// the gather form.
+template <int R, int Q>
+__device__ __forceinline__ void col_scatter(const float2* __restrict__ hin, float2 (&st)[2 * R], float* out, bool store,
+                                            const Params& pp) {
+    constexpr int RS = kTW + 2;
+#pragma unroll
+    for (int r = 0; r < Q; ++r) {
+        const float2 v = hin[r * RS];
+        const float2 o = ffma2(v, pp.taps_col[R], st[0]);
+#pragma unroll
+        for (int i = 0; i < 2 * R - 1; ++i) {
+            const int d = R - 1 - i;
+            st[i] = ffma2(v, pp.taps_col[d >= 0 ? d : -d], st[i + 1]);
+        }
+        st[2 * R - 1] = __fmul2_rn(v, make_float2(pp.taps_col[R], pp.taps_col[R]));
+        if (store) {  // planar: [channel][q][TW]
+            out[r * kTW] = o.x;
+            out[(Q + r) * kTW] = o.y;
+        }
+    }
+}
 
 // Per-segment geometry shared by every role.
 struct Segment {
     int frame, x0, ya, yb, a0, steps;
 };
 
-template <int R, int NKR>
-__global__ void __launch_bounds__(kRoles * (1 + 2 * NKR) * kItemsPerPair + kExtraThreads, 1)
-    fbf_fused_kernel(const __grid_constant__ Params p) {
-    using G = Geometry<R>;
+// Warp slots: [ROW np | COL np | COMB 4 | GEN np | LOAD 1]. Handoffs are
+// full/empty mbarrier pairs with per-warp arrivals:
+//   LOAD -fs-> GEN -gen-> ROW p -ring p-> COL p -col-> COMB
+template <int R, int Q, int NKR, int M>
+__global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_kernel(const __grid_constant__ Params p) {
+    using G = Geometry<R, Q, M>;
     constexpr int GW = G::GW, GS = G::GS, FSW = G::FSW, RB = G::RB, RBP = G::RBP, RROWS = G::RROWS, RS = G::RS;
-    constexpr int NFS = G::NFS, NGB = G::NGB, NCB = G::NCB;
+    constexpr int NFS = G::NFS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int np = p.n_pairs;
+    const int np = p.n_pairs, ngb = p.ngb, ncb = p.ncb;
     float* fstage = reinterpret_cast<float*>(smem_raw);                         // [NFS][Q][FSW]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + G::fstage_bytes);
-    uint64_t* fs_full = bars;                                // [NFS] LOAD -> GEN
-    uint64_t* fs_empty = fs_full + NFS;                      // [NFS] GEN  -> LOAD
-    uint64_t* gen_full = fs_empty + NFS;                     // [NGB] GEN  -> PAIR
-    uint64_t* gen_empty = gen_full + NGB;                    // [NGB] PAIR -> GEN
-    uint64_t* col_full = gen_empty + NGB;                    // [NCB] PAIR -> COMB
-    uint64_t* col_empty = col_full + NCB;                    // [NCB] COMB -> PAIR
-    unsigned int* s_fallbacks = reinterpret_cast<unsigned int*>(col_empty + NCB);
-    float2* gen = reinterpret_cast<float2*>(smem_raw + G::fstage_bytes + G::misc_bytes);  // [NGB][np][Q][GS]
-    float* colout = reinterpret_cast<float*>(gen + (size_t)NGB * np * kQ * GS);          // [NCB][np][Q][2][TW]
-    float2* ring = reinterpret_cast<float2*>(colout + (size_t)NCB * np * kQ * 2 * kTW);  // [np][RROWS][RS]
+    uint64_t* fs_full = bars;                                // [NFS] LOAD -> GEN (cp.async completion)
+    uint64_t* ring_full = fs_full + NFS;                     // [np][RBP] ROW p -> COL p (split mode)
+    uint64_t* ring_empty = ring_full + kMaxPairs * RBP;      // [np][RBP] COL p -> ROW p
+    float2* gen = reinterpret_cast<float2*>(smem_raw + G::fixed_bytes);  // [ngb][np][Q][GS]
+    float2* colout = gen + (size_t)ngb * np * Q * GS;                    // [ncb][np] x [2][Q][TW] floats
+    float2* ring = colout + (size_t)ncb * np * Q * kTW;                  // [np][RROWS][RS]
 
-    const int nrole = np * kItemsPerPair;  // threads of the PAIR and GEN roles
-    // Warp slots: [PAIR | COMB | GEN | LOAD]; the scheduler favours higher warp ids,
-    // so the latency-bound chains (GEN, COMB) get first pick of the issue slots and the
-    // FFMA2 streams of the pair warps fill the rest.
-    int role, tid;  // role: 0 GEN, 1 PAIR, 3 LOAD, 4 COMB
+    const int nrole = np * 32;  // threads of each of the ROW/PAIR and COL roles
+    const int nf = G::PAIR ? nrole : 2 * nrole;  // FFMA2 threads
+    int role, tid;  // Role; ROW is PAIR in pair mode
     {
-        const int t = threadIdx.x;
-        if (t < nrole)                          { role = 1; tid = t; }
-        else if (t < nrole + kCombThreads)      { role = 4; tid = t - nrole; }
-        else if (t < 2 * nrole + kCombThreads)  { role = 0; tid = t - nrole - kCombThreads; }
-        else                                    { role = 3; tid = t - 2 * nrole - kCombThreads; }
+        // Roles are numbered from the LAST warp down: the FFMA2 warps get the highest
+        // warp ids, which the issue arbiter of a sub-partition serves first; the
+        // latency-bound roles (gen, combine, loader) have slack and fill the gaps.
+        const int t = (blockDim.x / 32 - 1 - (int)(threadIdx.x / 32)) * 32 + (threadIdx.x & 31);
+        constexpr int CG = kCombThreads + kGenThreads;
+        if (t < nrole)                     { role = kRoleRow; tid = t; }
+        else if (t < nf)                   { role = kRoleCol; tid = t - nrole; }
+        else if (t < nf + kCombThreads)    { role = kRoleComb; tid = t - nf; }
+        else if (t < nf + CG)              { role = kRoleGen; tid = t - nf - kCombThreads; }
+        else                               { role = kRoleLoad; tid = t - nf - CG; }
     }
     const int lane = threadIdx.x & 31;
     const int zk = p.k_lo == 0 ? 1 : 0;  // k = 0 contributes the single pair (f, 1)
+    // named-barrier thread counts: producers + consumers of each handoff
+    const int gen_threads = kGenThreads + nrole;   // GEN -> ROW/PAIR and back
+    const int col_threads = nrole + kCombThreads;  // COL/PAIR -> COMB and back
+    constexpr int kFsThreads = kGenThreads + 32;   // GEN -> LOAD (f stage empty)
+#ifdef FBF_PHASES
+    long long _pw[2] = {0, 0};
+    const long long _pt0 = clock64();
+#endif
+    unsigned n_fallbacks = 0;  // combine threads: fallback pixels (filter.cpp:203-208)
     if (threadIdx.x == 0) {
-        *s_fallbacks = 0u;
-        // every warp arrives on its own (no intra-role barrier): counts = warps
-        const unsigned nw = (unsigned)np, ncw = kCombThreads / 32;
-        for (int b = 0; b < NFS; ++b) { mbar_init(&fs_full[b], 1); mbar_init(&fs_empty[b], nw); }
-        for (int b = 0; b < NGB; ++b) { mbar_init(&gen_full[b], nw); mbar_init(&gen_empty[b], nw); }
-        for (int b = 0; b < NCB; ++b) { mbar_init(&col_full[b], nw); mbar_init(&col_empty[b], ncw); }
+        for (int b = 0; b < NFS; ++b) mbar_init(&fs_full[b], 1);
+        for (int b = 0; b < np * RBP; ++b) { mbar_init(&ring_full[b], 1); mbar_init(&ring_empty[b], 1); }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-#ifdef FBF_PHASES
-    const long long _cta_t0 = clock64();
-    unsigned long long _gt0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_gt0));
-#endif
 
     // this CTA's contiguous share of the (frame, strip, row) units
     const long long U = p.total_units;
     const long long u_begin = U * blockIdx.x / gridDim.x;
     const long long u_end = U * (blockIdx.x + 1) / gridDim.x;
     const long long per_frame = (long long)p.n_strips * p.out_rows;
-    // steps start e rows early so that output rows begin exactly at ya
-    constexpr int e = (kQ - (2 * R) % kQ) % kQ;
-    constexpr int s0 = (2 * R + e) / kQ;
+    // steps start e rows early so that output rows begin exactly at ya; the first
+    // s0 steps of a segment only fill the ring
+    constexpr int e = (Q - (2 * R) % Q) % Q;
+    constexpr int s0 = (2 * R + e) / Q;
+    static_assert(s0 == RB - 1, "warm-up steps fill all but one ring block");
     auto segment_at = [&](long long u, long long& next) {
         Segment sg;
         sg.frame = (int)(u / per_frame);
@@ -482,48 +457,77 @@ __global__ void __launch_bounds__(kRoles * (1 + 2 * NKR) * kItemsPerPair + kExtr
         sg.ya = p.out_row0 + row;
         sg.yb = sg.ya + len;
         sg.a0 = sg.ya - R - e;
-        sg.steps = s0 + (len + kQ - 1) / kQ;
+        sg.steps = s0 + (len + Q - 1) / Q;
         return sg;
     };
 
     // ---- GEN: channel pairs of step s of segment sg into gen buffer gb --------------
-    // item = it * nrole + tid covers the two adjacent pixels (q, xl), (q, xl + 1).
+    // item = it * kGenThreads + tid covers the two adjacent pixels (q, xl), (q, xl + 1).
     constexpr int HGW = GW / 2;  // GW = TW + 2R is even
-    constexpr int GITER = NKR > 0 ? (kQ * HGW + 2 * NKR * kItemsPerPair - 1) / (2 * NKR * kItemsPerPair)
-                                  : (kQ * HGW + kItemsPerPair - 1) / kItemsPerPair;
-    auto gen_step = [&](const Segment& sg, int s, int fb, int gb) {
-        const int a = sg.a0 + s * kQ;
-        const int xoff = (sg.x0 - R) - ((sg.x0 - R) & ~3);
-        const float* fs = fstage + fb * kQ * FSW + xoff;
-        float2* gbuf = gen + (size_t)gb * np * kQ * GS;
-        const int lo = max(a, sg.ya - R), hi = min(a + kQ, sg.yb + R);
-        const bool zb = p.border == 2;
-        const float inv = p.inv_period;
+    constexpr int GITER = (Q * HGW + kGenThreads - 1) / kGenThreads;
+    // Per-thread item geometry is fixed over steps and segments: the f staging
+    // offset (x0 - R is congruent to -R mod 4, so the staged row origin lies at a
+    // compile-time offset XOFF), the gen offset, and the row q (-1: no item).
+    constexpr int XOFF = ((-R) % 4 + 4) % 4;
+    struct GenItem {
+        int fso, go, q, xl;
+    };
+    auto gen_items = [&](GenItem (&gi)[GITER]) {
 #pragma unroll
         for (int it = 0; it < GITER; ++it) {
-            const int item = it * nrole + tid;
-            if (item < kQ * HGW) {
-                const int q = item / HGW, xl = 2 * (item - q * HGW);
-                const int gy = a + q, gx = sg.x0 - R + xl;
-                const bool rowok = gy >= lo && gy < hi && (!zb || (gy >= 0 && gy < p.height));
+            const int item = it * kGenThreads + tid;
+            const int q = item / HGW, xl = 2 * (item - q * HGW);
+            gi[it] = GenItem{q * FSW + xl + XOFF, q * GS + xl, item < Q * HGW ? q : -1, xl};
+        }
+    };
+    auto gen_step = [&](const Segment& sg, int s, int fb, int gb, const GenItem (&gi)[GITER]) {
+        const int a = sg.a0 + s * Q;
+        const float* fs = fstage + fb * Q * FSW;
+        float2* gbuf = gen + gb * np * Q * GS;
+        // rows of the step that feed an output row and (zero border) lie in the image
+        int lo = max(a, sg.ya - R), hi = min(a + Q, sg.yb + R);
+        const bool zb = p.border == 2;
+        if (zb) {
+            lo = max(lo, 0);
+            hi = min(hi, p.height);
+        }
+        const float inv = p.inv_period;
+        const int gx0 = sg.x0 - R;
+#pragma unroll 2
+        for (int it = 0; it < GITER; ++it) {
+            const int q = gi[it].q;
+            if (q >= 0) {
+                const bool rowok = a + q >= lo && a + q < hi;
+                const int gx = gx0 + gi[it].xl;
                 const bool va = rowok && (!zb || (gx >= 0 && gx < p.width));
                 const bool vb = rowok && (!zb || (gx + 1 >= 0 && gx + 1 < p.width));
-                const float2 f = make_float2(va ? fs[q * FSW + xl] : 0.f, vb ? fs[q * FSW + xl + 1] : 0.f);
-                float4* gp = reinterpret_cast<float4*>(gbuf + q * GS + xl);
-                if (zk) gp[0] = make_float4(f.x, va ? 1.f : 0.f, f.y, vb ? 1.f : 0.f);
+                const float2 f = make_float2(va ? fs[gi[it].fso] : 0.f, vb ? fs[gi[it].fso + 1] : 0.f);
+                // per pixel (first, second) channel pairs, stored as float2 at gp[0] / gp[1]
+                float2* gp = gbuf + gi[it].go;
+                if (zk) {
+                    gp[0] = make_float2(f.x, va ? 1.f : 0.f);
+                    gp[1] = make_float2(f.y, vb ? 1.f : 0.f);
+                }
                 if (NKR > 0) {
-                    const CS2 c1 = harmonic1x2(f, inv);
-                    const float2 nws = make_float2(-c1.s.x, -c1.s.y);
-                    CS2 cs = p.k_first > 1 ? harmonic_first2(c1, p.k_first) : c1;
-                    if (!va) cs.c.x = cs.s.x = 0.f;
-                    if (!vb) cs.c.y = cs.s.y = 0.f;
-                    float4* gk = gp + (size_t)zk * kQ * GS / 2;
+                    const CS2 h = harmonic1x2(f, inv);
+                    const float2 w0 = make_float2(h.c.x, h.s.x), w1 = make_float2(h.c.y, h.s.y);
+                    float2 z0 = p.k_first > 1 ? harmonic_first1(w0, p.k_first) : w0;
+                    float2 z1 = p.k_first > 1 ? harmonic_first1(w1, p.k_first) : w1;
+                    if (!va) z0 = make_float2(0.f, 0.f);
+                    if (!vb) z1 = make_float2(0.f, 0.f);
+                    float2* gk = gp + zk * (Q * GS);
 #pragma unroll
                     for (int kk = 0; kk < NKR; ++kk) {
-                        const float2 cf = __fmul2_rn(cs.c, f), sf = __fmul2_rn(cs.s, f);
-                        gk[(size_t)(2 * kk) * kQ * GS / 2] = make_float4(cf.x, sf.x, cf.y, sf.y);
-                        gk[(size_t)(2 * kk + 1) * kQ * GS / 2] = make_float4(cs.c.x, cs.s.x, cs.c.y, cs.s.y);
-                        if (kk + 1 < NKR) cs = rotate2(cs, c1, nws);
+                        float2* pf = gk + (2 * kk) * (Q * GS);      // (C_k f, S_k f)
+                        float2* pc = gk + (2 * kk + 1) * (Q * GS);  // (C_k, S_k)
+                        pf[0] = __fmul2_rn(z0, make_float2(f.x, f.x));
+                        pf[1] = __fmul2_rn(z1, make_float2(f.y, f.y));
+                        pc[0] = z0;
+                        pc[1] = z1;
+                        if (kk + 1 < NKR) {
+                            z0 = rotate1(z0, w0);
+                            z1 = rotate1(z1, w1);
+                        }
                     }
                 }
             }
@@ -531,75 +535,108 @@ __global__ void __launch_bounds__(kRoles * (1 + 2 * NKR) * kItemsPerPair + kExtr
     };
 
     // ---- COMB: combine of step s of segment sg from column buffer cb -----------------
-    // one item = two adjacent output pixels per thread; f is re-read from the source
-    // image (L2-resident) so nothing but the column results travels through smem
-    auto combine_step = [&](const Segment& sg, int s, int cb) {
-        const int a = sg.a0 + s * kQ;
-        constexpr int HTW = kTW / 2;
-        static_assert(kCombThreads == kQ * HTW, "one combine item per thread");
-        const int q = tid / HTW, x = 2 * (tid - q * HTW);
-        const int y = a - R + q, gxo = sg.x0 + x;
-        if (y >= sg.yb || gxo >= p.width) return;
-        const bool vb = gxo + 1 < p.width;
-        const float* srow = p.src + (long long)sg.frame * p.src_frame_stride + (long long)(y - p.src_row0) * p.src_pitch;
-        const float2 f = make_float2(__ldg(srow + gxo), vb ? __ldg(srow + gxo + 1) : 0.f);
-        // validate_intensities (filter.cpp:19-23): every pixel is an output pixel exactly once
-        if (p.bad_pixels && !(f.x >= 0.f && f.x <= p.range_max && f.y >= 0.f && f.y <= p.range_max))
-            atomicOr(p.bad_pixels, 1u);
-        float* dst = p.dst + (long long)sg.frame * p.dst_frame_stride;
-        float2* acc = p.acc ? p.acc + (long long)sg.frame * p.acc_frame_stride : nullptr;
-        float2 num = make_float2(0.f, 0.f), den = make_float2(0.f, 0.f);
-        const long long ai = (long long)(y - p.out_row0) * p.width + gxo;
-        if (!p.first_chunk) {
-            const float2 nda = acc[ai], ndb = vb ? acc[ai + 1] : make_float2(0.f, 0.f);
-            num = make_float2(nda.x, ndb.x);
-            den = make_float2(nda.y, ndb.y);
-        }
-        // planar column results: [pair][q][component][TW]
-        const float* go = colout + (size_t)cb * np * kQ * 2 * kTW + q * 2 * kTW + x;
-        constexpr int PSTR = kQ * 2 * kTW;  // floats per pair
-        if (zk) {
-            const float2 gx0 = *reinterpret_cast<const float2*>(go);
-            const float2 gy0 = *reinterpret_cast<const float2*>(go + kTW);
-            const float2 c0 = make_float2(p.coeff[0], p.coeff[0]);
-            num = __ffma2_rn(c0, gx0, num);
-            den = __ffma2_rn(c0, gy0, den);
-        }
-        if (NKR > 0) {
-            const CS2 c1 = harmonic1x2(f, p.inv_period);
-            const float2 nws = make_float2(-c1.s.x, -c1.s.y);
-            CS2 cs = p.k_first > 1 ? harmonic_first2(c1, p.k_first) : c1;
-            const float* gk = go + zk * PSTR;
+    // one item = two adjacent output pixels; f is re-read from the source image
+    // (L2-resident) so nothing but the column results travels through smem
+    constexpr int HTW = kTW / 2;
+    constexpr int CITER = Q * HTW / kCombThreads;
+    static_assert(CITER * kCombThreads == Q * HTW, "combine items tile the step");
+    // Per-thread items: pointers to the item's pixels in the first output step
+    // of the segment, advanced by Q rows per step.
+    struct CombItem {
+        const float* sp;  // f
+        float* dp;        // output
+        float2* ap;       // (num, den) scratch
+        int co;           // column-result offset (float2) within a pair's tile
+        int y;            // output row of the current step
+        bool colok, vb;   // pixel pair in the image / second pixel in the image
+    };
+    auto comb_items = [&](const Segment& sg, CombItem (&ci)[CITER]) {
 #pragma unroll
-            for (int kk = 0; kk < NKR; ++kk) {
-                const float2 ck = make_float2(p.coeff[zk + kk], p.coeff[zk + kk]);
-                const float* gn = gk + (2 * kk) * PSTR;
-                const float* gd = gk + (2 * kk + 1) * PSTR;
-                const float2 gnx = *reinterpret_cast<const float2*>(gn);
-                const float2 gny = *reinterpret_cast<const float2*>(gn + kTW);
-                const float2 gdx = *reinterpret_cast<const float2*>(gd);
-                const float2 gdy = *reinterpret_cast<const float2*>(gd + kTW);
-                num = __ffma2_rn(ck, __ffma2_rn(cs.s, gny, __fmul2_rn(cs.c, gnx)), num);
-                den = __ffma2_rn(ck, __ffma2_rn(cs.s, gdy, __fmul2_rn(cs.c, gdx)), den);
-                if (kk + 1 < NKR) cs = rotate2(cs, c1, nws);
-            }
+        for (int it = 0; it < CITER; ++it) {
+            const int item = it * kCombThreads + tid;
+            const int q = item / HTW, x = 2 * (item - q * HTW);
+            const int gxo = sg.x0 + x, y = sg.a0 + s0 * Q - R + q;
+            ci[it].co = q * kTW + x;
+            ci[it].y = y;
+            ci[it].colok = gxo < p.width;
+            ci[it].vb = gxo + 1 < p.width;
+            ci[it].sp = p.src + (long long)sg.frame * p.src_frame_stride + (long long)(y - p.src_row0) * p.src_pitch + gxo;
+            ci[it].dp = p.dst + (long long)sg.frame * p.dst_frame_stride + (long long)(y - p.out_row0) * p.dst_pitch + gxo;
+            ci[it].ap = p.acc ? p.acc + (long long)sg.frame * p.acc_frame_stride + (long long)(y - p.out_row0) * p.width + gxo
+                              : nullptr;
         }
-        float* drow = dst + (long long)(y - p.out_row0) * p.dst_pitch + gxo;
-        if (p.last_chunk) {
-            float oa = f.x, ob = f.y;
-            unsigned nfb = 0;
-            if (den.x > 1e-12f) oa = __fdividef(num.x, den.x); else ++nfb;
-            if (den.y > 1e-12f) ob = __fdividef(num.y, den.y); else nfb += vb;
-            if (nfb) atomicAdd(s_fallbacks, nfb);
-            drow[0] = oa;
-            if (vb) drow[1] = ob;
-        } else {
-            acc[ai] = make_float2(num.x, den.x);
-            if (vb) acc[ai + 1] = make_float2(num.y, den.y);
+    };
+    // f of the step's output pixels, loaded before the step's column results are
+    // waited for so that the L2 latency overlaps the wait
+    auto combine_load = [&](const Segment& sg, const CombItem (&ci)[CITER], float2 (&fv)[CITER]) {
+#pragma unroll
+        for (int it = 0; it < CITER; ++it) {
+            fv[it] = make_float2(0.f, 0.f);
+            if (ci[it].y < sg.yb && ci[it].colok) fv[it] = make_float2(__ldg(ci[it].sp), ci[it].vb ? __ldg(ci[it].sp + 1) : 0.f);
+        }
+    };
+    auto combine_step = [&](const Segment& sg, int cb, CombItem (&ci)[CITER], const float2 (&fv)[CITER]) {
+        const float* cbase = reinterpret_cast<const float*>(colout + cb * np * Q * kTW);
+#pragma unroll
+        for (int it = 0; it < CITER; ++it) {
+            CombItem& c = ci[it];
+            if (c.y < sg.yb && c.colok) {
+                const bool vb = c.vb;
+                const float2 f = fv[it];
+                // validate_intensities (filter.cpp:19-23): every pixel is an output pixel exactly once
+                if (p.bad_pixels && !(f.x >= 0.f && f.x <= p.range_max && f.y >= 0.f && f.y <= p.range_max))
+                    atomicOr(p.bad_pixels, 1u);
+                float2 num = make_float2(0.f, 0.f), den = make_float2(0.f, 0.f);
+                if (!p.first_chunk) {
+                    const float2 nda = c.ap[0], ndb = vb ? c.ap[1] : make_float2(0.f, 0.f);
+                    num = make_float2(nda.x, ndb.x);
+                    den = make_float2(nda.y, ndb.y);
+                }
+                // planar column results [pair][channel][q][TW]: float2 = the two pixels of one channel
+                const float2* go = reinterpret_cast<const float2*>(cbase + c.co);
+                constexpr int CSTR = Q * kTW / 2;  // float2 per channel plane
+                if (zk) {
+                    const float2 c0 = make_float2(p.coeff[0], p.coeff[0]);
+                    num = __ffma2_rn(c0, go[0], num);
+                    den = __ffma2_rn(c0, go[CSTR], den);
+                }
+                if (NKR > 0) {
+                    const CS2 c1 = harmonic1x2(f, p.inv_period);
+                    CS2 cs = p.k_first > 1 ? harmonic_first2(c1, p.k_first) : c1;
+                    const float2* gk = go + zk * 2 * CSTR;
+#pragma unroll
+                    for (int kk = 0; kk < NKR; ++kk) {
+                        const float2 ck = make_float2(p.coeff[zk + kk], p.coeff[zk + kk]);
+                        const float2* pn = gk + (4 * kk) * CSTR;  // G(C_k f), G(S_k f)
+                        const float2* pd = pn + 2 * CSTR;         // G(C_k), G(S_k)
+                        num = __ffma2_rn(ck, __ffma2_rn(cs.s, pn[CSTR], __fmul2_rn(cs.c, pn[0])), num);
+                        den = __ffma2_rn(ck, __ffma2_rn(cs.s, pd[CSTR], __fmul2_rn(cs.c, pd[0])), den);
+                        if (kk + 1 < NKR) cs = rotate2(cs, c1);
+                    }
+                }
+                if (p.last_chunk) {
+                    float oa = f.x, ob = f.y;
+                    unsigned nfb = 0;
+                    if (den.x > 1e-12f) oa = __fdividef(num.x, den.x); else ++nfb;
+                    if (den.y > 1e-12f) ob = __fdividef(num.y, den.y); else nfb += vb;
+                    n_fallbacks += nfb;
+                    c.dp[0] = oa;
+                    if (vb) c.dp[1] = ob;
+                } else {
+                    c.ap[0] = make_float2(num.x, den.x);
+                    if (vb) c.ap[1] = make_float2(num.y, den.y);
+                }
+            }
+            c.y += Q;
+            c.sp += (long long)Q * p.src_pitch;
+            c.dp += (long long)Q * p.dst_pitch;
+            if (c.ap) c.ap += (long long)Q * p.width;
         }
     };
 
-    int gstep = 0;  // global step counter: buffers are used round-robin over it
+    auto run_roles = [&](auto fma_region) {
+    constexpr bool FMA = decltype(fma_region)::value;
+    int gstep = 0;  // global step counter: buffers and ring blocks are used round-robin over it
     for (long long u = u_begin; u < u_end;) {
         long long next;
         const Segment sg = segment_at(u, next);
@@ -608,18 +645,21 @@ __global__ void __launch_bounds__(kRoles * (1 + 2 * NKR) * kItemsPerPair + kExtr
         const int x0 = sg.x0, ya = sg.ya, yb = sg.yb, a0 = sg.a0;
         const int xs = (x0 - R) & ~3;  // f staging row origin (16-byte aligned)
 
-        if (role == 3) {
+        if (role == kRoleLoad) {
             // ============================ LOAD ==============================
             // fstage row q holds f at columns [xs, xs + FSW), border-mapped with
             // 4-byte cp.async (or one TMA bulk copy per row for the in-image span,
             // FBF_STAGE=bulk). Zero-border rows/columns outside the image are never
             // read: GEN treats them as zero.
             const float* src = p.src + (long long)sg.frame * p.src_frame_stride;
+            // interior strips: the staged window [xs, xs + FSW) lies in the image and
+            // rows are 16-byte aligned -> whole rows with 16-byte cp.async
+            const bool vec = p.vec_ok && !p.use_tma && xs >= 0 && xs + FSW <= p.width;
             const int c0 = max(xs, 0), c1 = min(xs + FSW, p.width);  // in-image span
             const bool bulk = p.use_tma && c1 > c0;
             constexpr int LCOLS = (GW + 31) / 32;
             int lmx[LCOLS], loff[LCOLS];
-            {
+            if (!vec) {
                 const int wlo = x0 - R, whi = x0 + kTW + R;
                 const int blo = bulk ? c0 : whi, bhi = bulk ? c1 : whi;  // bulk-covered span
                 const int nleft = max(0, min(blo, whi) - wlo), nright = max(0, whi - max(bhi, wlo));
@@ -635,141 +675,217 @@ __global__ void __launch_bounds__(kRoles * (1 + 2 * NKR) * kItemsPerPair + kExtr
             for (int s = 0; s < steps; ++s) {
                 const int g = gstep + s;
                 const int fb = g % NFS;
-                if (g >= NFS) mbar_wait(&fs_empty[fb], (unsigned)((g / NFS - 1) & 1));
-                float* fs = fstage + fb * kQ * FSW;
-                const int a = a0 + s * kQ;
-                const int lo = max(a, ya - R), hi = min(a + kQ, yb + R);
+                if (g >= NFS) PSYNC(0, kBarFsEmpty + fb, kFsThreads);
+                float* fs = fstage + fb * Q * FSW;
+                const int a = a0 + s * Q;
+                const int lo = max(a, ya - R), hi = min(a + Q, yb + R);
 #ifdef FBF_SKIP_LOAD
                 if (tid == 0) mbar_arrive(&fs_full[fb]);
                 continue;
 #endif
-                if (bulk) {
-                    int nrows_src = 0;  // needed rows that read the image
-                    for (int gy = lo; gy < hi; ++gy) nrows_src += map_border(gy, p.height, p.border) >= 0;
-                    if (tid == 0 && nrows_src > 0)
-                        mbar_expect_tx(&fs_full[fb], (unsigned)(sizeof(float) * (c1 - c0) * nrows_src));
-                    __syncwarp();
-                    if (tid < kQ) {
-                        const int gy = a + tid;
-                        const int my = (gy >= lo && gy < hi) ? map_border(gy, p.height, p.border) : -1;
-                        if (my >= 0)
-                            tma_bulk_g2s(fs + tid * FSW + (c0 - xs),
-                                         src + (long long)(my - p.src_row0) * p.src_pitch + c0,
-                                         (unsigned)(sizeof(float) * (c1 - c0)), &fs_full[fb]);
+                if (vec) {
+                    constexpr int NV = FSW / 4;  // float4 per staged row
+                    constexpr int VITER = (Q * NV + 31) / 32;
+#pragma unroll 1
+                    for (int it = 0; it < VITER; ++it) {
+                        const int i = it * 32 + tid;
+                        if (i < Q * NV) {
+                            const int q = i / NV, c = i - q * NV;
+                            const int gy = a + q;
+                            const int my = (gy >= lo && gy < hi) ? map_border(gy, p.height, p.border) : -1;
+                            if (my >= 0)
+                                cp_async16(fs + q * FSW + 4 * c, src + (long long)(my - p.src_row0) * p.src_pitch + xs + 4 * c);
+                        }
                     }
-                }
+                } else {
+                    if (bulk) {
+                        int nrows_src = 0;  // needed rows that read the image
+                        for (int gy = lo; gy < hi; ++gy) nrows_src += map_border(gy, p.height, p.border) >= 0;
+                        if (tid == 0 && nrows_src > 0)
+                            mbar_expect_tx(&fs_full[fb], (unsigned)(sizeof(float) * (c1 - c0) * nrows_src));
+                        __syncwarp();
+                        if (tid < Q) {
+                            const int gy = a + tid;
+                            const int my = (gy >= lo && gy < hi) ? map_border(gy, p.height, p.border) : -1;
+                            if (my >= 0)
+                                tma_bulk_g2s(fs + tid * FSW + (c0 - xs),
+                                             src + (long long)(my - p.src_row0) * p.src_pitch + c0,
+                                             (unsigned)(sizeof(float) * (c1 - c0)), &fs_full[fb]);
+                        }
+                    }
 #pragma unroll
-                for (int q = 0; q < kQ; ++q) {
-                    const int gy = a + q;
-                    const int my = (gy >= lo && gy < hi) ? map_border(gy, p.height, p.border) : -1;
-                    if (my < 0) continue;
-                    const float* srow = src + (long long)(my - p.src_row0) * p.src_pitch;
+                    for (int q = 0; q < Q; ++q) {
+                        const int gy = a + q;
+                        const int my = (gy >= lo && gy < hi) ? map_border(gy, p.height, p.border) : -1;
+                        if (my < 0) continue;
+                        const float* srow = src + (long long)(my - p.src_row0) * p.src_pitch;
 #pragma unroll
-                    for (int j = 0; j < LCOLS; ++j)
-                        if (lmx[j] >= 0) cp_async4(fs + q * FSW + loff[j], srow + lmx[j]);
+                        for (int j = 0; j < LCOLS; ++j)
+                            if (lmx[j] >= 0) cp_async4(fs + q * FSW + loff[j], srow + lmx[j]);
+                    }
                 }
                 cp_async_mbar_arrive(&fs_full[fb]);
                 __syncwarp();
                 if (tid == 0) mbar_arrive(&fs_full[fb]);
             }
-        } else if (role == 0) {
+        } else if (role == kRoleGen) {
             // ============================= GEN ==============================
-            FBF_PHASE_T0();
+            GenItem gi[GITER];
+            gen_items(gi);
             for (int t = 0; t < steps; ++t) {
                 const int g = gstep + t;
-                const int fb = g % NFS, gb = g % NGB;
-                FBF_PHASE(0);
-                mbar_wait(&fs_full[fb], (unsigned)((g / NFS) & 1));
-                if (g >= NGB) mbar_wait(&gen_empty[gb], (unsigned)((g / NGB - 1) & 1));
-                FBF_PHASE(1);
+                const int fb = g % NFS, gb = g % ngb;
+                PWAIT(0, &fs_full[fb], (unsigned)((g / NFS) & 1));
+                if (g >= ngb) PSYNC(1, kBarGenEmpty + gb, gen_threads);
 #ifndef FBF_SKIP_GEN
-                gen_step(sg, t, fb, gb);
+                gen_step(sg, t, fb, gb, gi);
 #endif
-                FBF_PHASE(4);
-                __syncwarp();  // this warp's part of gen buffer gb written, fstage fb read
-                if (lane == 0) {
-                    mbar_arrive(&fs_empty[fb]);
-                    mbar_arrive(&gen_full[gb]);
-                }
-                FBF_PHASE(5);
+                // this warp's part of gen buffer gb written, fstage fb read
+                named_arrive(kBarFsEmpty + fb, kFsThreads);
+                named_arrive(kBarGenFull + gb, gen_threads);
             }
-        } else if (role == 4) {
+        } else if (role == kRoleComb) {
             // ============================ COMB ==============================
-            FBF_PHASE_T0();
-            for (int sc = 0; sc < steps; ++sc) {
-                const int g = gstep + sc;
-                const int cb = g % NCB;
-                mbar_wait(&col_full[cb], (unsigned)((g / NCB) & 1));
-                FBF_PHASE(12);
+            CombItem ci[CITER];
+            comb_items(sg, ci);
+            for (int t = 0; t < steps; ++t) {
+                const int g = gstep + t;
+                const int cb = g % ncb;
+                float2 fv[CITER];
+                if (t >= s0) combine_load(sg, ci, fv);
+                PSYNC(0, kBarColFull + cb, col_threads);
 #ifndef FBF_SKIP_COMB
-                if (sc >= s0) combine_step(sg, sc, cb);
+                if (t >= s0) combine_step(sg, cb, ci, fv);
 #endif
-                FBF_PHASE(13);
-                __syncwarp();  // this warp is done with column buffer cb
-                if (lane == 0) mbar_arrive(&col_empty[cb]);
+                named_arrive(kBarColEmpty + cb, col_threads);  // this warp is done with column buffer cb
             }
-        } else {
+        } else if (FMA && G::PAIR && role == kRoleRow) {
             // ============================= PAIR =============================
-            // iteration t: horizontal pass of step t + vertical pass of step t - 1
-            const int pr = tid / 32;  // this warp's channel pair
-            float2* myring = ring + (size_t)pr * RROWS * RS;
-            static_assert(kQ * (kTW / kP) == 32 && kQ == kP, "one pair = one warp");
-            FBF_PHASE_T0();
-            for (int t = 0; t <= steps; ++t) {
-                const bool do_row = t < steps;
-                const bool do_col = t >= 1 + s0;
-                const int g = gstep + t, gc = g - 1;
-                const int gb = g % NGB, cb = gc % NCB;
-                FBF_PHASE(2);
-                if (do_row) mbar_wait(&gen_full[gb], (unsigned)((g / NGB) & 1));
-                // column buffer cb must have been consumed by COMB even on warm-up steps:
-                // the arrival below completes a phase of col_full[cb], and a warp running
-                // ahead must not complete the phase of a step its siblings have not finished
-                if (t >= 1 && gc >= NCB) mbar_wait(&col_empty[cb], (unsigned)((gc / NCB - 1) & 1));
-                FBF_PHASE(3);
-                const float4* gin = reinterpret_cast<const float4*>(
-                    gen + (((size_t)gb * np + pr) * kQ + lane % kQ) * GS + (lane / kQ) * kP);
-                float* oc = colout + ((size_t)cb * np + pr) * kQ * 2 * kTW;
-                const int blk_row = g % RBP, blk_col = gc % RBP;
-                if (do_row && do_col)
-                    pair_iter<R, true, true>(gin, myring, blk_row, blk_col, lane, p.taps, oc, &gen_empty[gb]);
-                else if (do_row)
-                    pair_iter<R, true, false>(gin, myring, blk_row, blk_col, lane, p.taps, oc, &gen_empty[gb]);
-                else if (do_col)
-                    pair_iter<R, false, true>(gin, myring, blk_row, blk_col, lane, p.taps, oc, &gen_empty[gb]);
-                FBF_PHASE(6);
-                __syncwarp();  // ring block / column results of this warp complete
-                if (t >= 1 && lane == 0) mbar_arrive(&col_full[cb]);  // (warm-up steps hand over nothing)
-                FBF_PHASE(11);
+            // row pass of step t into the warp's own block, then the scatter column
+            // pass of the same rows; the 2R column partial sums stay in registers
+            if constexpr (FMA && G::PAIR) {
+                const int pr = tid / 32;
+                const int q = lane % Q, xc = lane / Q;
+                float2* hbuf = ring + (size_t)pr * RROWS * RS;
+                float2 st[2 * R];
+#pragma unroll
+                for (int i = 0; i < 2 * R; ++i) st[i] = make_float2(0.f, 0.f);  // new segment
+                for (int t = 0; t < steps; ++t) {
+                    const int g = gstep + t;
+                    const int gb = g % ngb, cb = g % ncb;
+                    PSYNC(0, kBarGenFull + gb, gen_threads);
+                    const float4* gin =
+                        reinterpret_cast<const float4*>(gen + (((size_t)gb * np + pr) * Q + q) * GS + xc * Q);
+                    row_pass<R, Q>(gin, reinterpret_cast<float4*>(hbuf + (size_t)q * RS + xc * Q), p,
+                                   kBarGenEmpty + gb, gen_threads);
+                    __syncwarp();  // the step's row-pass block is complete
+                    // column buffer cb must have been consumed by COMB even on warm-up steps:
+                    // the arrival below completes a phase of col_full[cb]
+                    if (g >= ncb) PSYNC(1, kBarColEmpty + cb, col_threads);
+                    col_scatter<R, Q>(hbuf + lane, st, reinterpret_cast<float*>(colout + ((size_t)cb * np + pr) * Q * kTW) + lane, t >= s0,
+                                      p);
+                    named_arrive(kBarColFull + cb, col_threads);
+                }
+            }
+        } else if (FMA && role == kRoleRow) {
+            // ============================= ROW ==============================
+            if constexpr (FMA && !G::PAIR) {
+                const int pr = tid / 32;  // this warp's channel pair
+                const int q = lane % Q, xc = lane / Q;
+                static_assert(Q * (kTW / Q) == 32, "one warp covers a step of one pair");
+                float2* myring = ring + (size_t)pr * RROWS * RS;
+                for (int t = 0; t < steps; ++t) {
+                    const int g = gstep + t;
+                    const int gb = g % ngb, blk = g % RBP;
+                    PSYNC(0, kBarGenFull + gb, gen_threads);
+                    // ring block blk last held step g - RBP, read up to column pass g - RBP + RBN - 1
+                    if (g >= RBP) PWAIT(1, &ring_empty[pr * RBP + blk], (unsigned)((g / RBP - 1) & 1));
+                    const float4* gin = reinterpret_cast<const float4*>(gen + (((size_t)gb * np + pr) * Q + q) * GS + xc * Q);
+                    float4* hout = reinterpret_cast<float4*>(myring + ((size_t)blk * Q + q) * RS + xc * Q);
+                    row_pass<R, Q>(gin, hout, p, kBarGenEmpty + gb, gen_threads);
+                    __syncwarp();  // ring block complete
+                    if (lane == 0) mbar_arrive(&ring_full[pr * RBP + blk]);
+                }
+            }
+        } else if (FMA && role == kRoleCol) {
+            // ============================= COL ==============================
+            const int pr = tid / 32;
+            const float2* myring = ring + (size_t)pr * RROWS * RS;
+            if constexpr (!FMA || G::PAIR) {
+            } else if constexpr (G::SCATTER) {
+                float2 st[2 * R];
+#pragma unroll
+                for (int i = 0; i < 2 * R; ++i) st[i] = make_float2(0.f, 0.f);  // new segment
+                for (int t = 0; t < steps; ++t) {
+                    const int g = gstep + t;
+                    const int blk = g % RBP, cb = g % ncb;
+                    PWAIT(0, &ring_full[pr * RBP + blk], (unsigned)((g / RBP) & 1));
+                    // column buffer cb must have been consumed by COMB even on warm-up steps:
+                    // the arrival below completes a phase of col_full[cb]
+                    if (g >= ncb) PSYNC(1, kBarColEmpty + cb, col_threads);
+                    col_scatter<R, Q>(myring + (size_t)blk * Q * RS + lane, st,
+                                      reinterpret_cast<float*>(colout + ((size_t)cb * np + pr) * Q * kTW) + lane, t >= s0, p);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&ring_empty[pr * RBP + blk]);  // block free for row pass g + RBP
+                    named_arrive(kBarColFull + cb, col_threads);
+                }
+            } else {
+                for (int t = 0; t < steps; ++t) {
+                    const int g = gstep + t;
+                    const int blk = g % RBP, cb = g % ncb;
+                    const bool do_col = t >= s0;
+                    PWAIT(0, &ring_full[pr * RBP + blk], (unsigned)((g / RBP) & 1));
+                    float2 acc[Q];
+                    if (do_col) col_pass<R, Q>(myring, blk, lane, p, acc);
+                    __syncwarp();
+                    // the oldest block of the window (step g - RB + 1) is free for row pass g - RB + 1 + RBP
+                    if (lane == 0 && g >= RB - 1) mbar_arrive(&ring_empty[pr * RBP + (g - RB + 1) % RBP]);
+                    // column buffer cb must have been consumed by COMB even on warm-up steps:
+                    // the arrival below completes a phase of col_full[cb]
+                    if (g >= ncb) PSYNC(1, kBarColEmpty + cb, col_threads);
+                    if (do_col) {
+                        float* oc = reinterpret_cast<float*>(colout + ((size_t)cb * np + pr) * Q * kTW) + lane;
+#pragma unroll
+                        for (int o = 0; o < Q; ++o) {  // planar: [channel][q][TW]
+                            oc[o * kTW] = acc[o].x;
+                            oc[(Q + o) * kTW] = acc[o].y;
+                        }
+                    }
+                    named_arrive(kBarColFull + cb, col_threads);
+                }
             }
         }
         gstep += steps;
     }
-    __syncthreads();
+    };  // run_roles
+    run_roles(std::true_type{});
+    if (role == kRoleComb && p.fallbacks) {
+        const unsigned w = __reduce_add_sync(0xffffffffu, n_fallbacks);
+        if (lane == 0 && w) atomicAdd(p.fallbacks, (unsigned long long)w);
+    }
 #ifdef FBF_PHASES
-    if (threadIdx.x == 0) {
-        unsigned long long _gt1;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_gt1));
-        atomicMax(&g_phase_cycles[14], (unsigned long long)(clock64() - _cta_t0));
-        atomicAdd(&g_phase_cycles[15], (unsigned long long)(clock64() - _cta_t0) * 1000ull / (_gt1 - _gt0 + 1));
-        if (blockIdx.x < 1024) g_cta_cycles[blockIdx.x] = (unsigned long long)(clock64() - _cta_t0);
+    if (p.prof && lane == 0) {
+        unsigned long long* pw = p.prof + 4 * (threadIdx.x / 32);
+        atomicAdd(pw + 0, (unsigned long long)(clock64() - _pt0));
+        atomicAdd(pw + 1, (unsigned long long)_pw[0]);
+        atomicAdd(pw + 2, (unsigned long long)_pw[1]);
+        atomicAdd(pw + 3, 1ull);
     }
 #endif
-    if (threadIdx.x == 0 && p.fallbacks && *s_fallbacks) atomicAdd(p.fallbacks, (unsigned long long)*s_fallbacks);
 }
 
-template <int R, int NKR>
+template <int R, int Q, int NKR, int M>
 cudaError_t launch_fused(const Params& p, int grid, cudaStream_t stream) {
-    using G = Geometry<R>;
-    const size_t smem = G::smem_bytes(p.n_pairs);
+    using G = Geometry<R, Q, M>;
+    const size_t smem = G::smem_bytes(p.n_pairs, p.ngb, p.ncb);
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fbf_fused_kernel<R, NKR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)kSmemLimit);
+        cudaError_t e = cudaFuncSetAttribute(fbf_fused_kernel<R, Q, NKR, M>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    fbf_fused_kernel<R, NKR><<<grid, kRoles * p.n_pairs * kItemsPerPair + kExtraThreads, smem, stream>>>(p);
+    fbf_fused_kernel<R, Q, NKR, M><<<grid, block_threads(p.n_pairs, M), smem, stream>>>(p);
     return cudaGetLastError();
 }
 
