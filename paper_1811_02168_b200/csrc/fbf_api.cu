@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -436,9 +437,21 @@ int filter_frames_on_device(int dev, const float* img, int n_frames, int width, 
     for (int i = 0; i <= pieces; ++i) lo[i] = (int)((long long)extent * i / pieces);
     const size_t unit = bands ? (size_t)width : fp;  // floats per row / per frame
     cudaEvent_t ev;
+    // dev: FBF_TRACE=1 prints the stage timeline of this call (timing events)
+    static const bool trace = std::getenv("FBF_TRACE") != nullptr;
+    std::vector<std::pair<const char*, cudaEvent_t>> tl;
+    auto mark = [&](const char* what, cudaStream_t st) {
+        if (!trace) return;
+        cudaEvent_t e;
+        cudaEventCreateWithFlags(&e, cudaEventDefault);
+        cudaEventRecord(e, st);
+        tl.emplace_back(what, e);
+    };
+    mark("start", si);
     for (int i = 0; i < pieces; ++i) {
         const size_t off = (size_t)lo[i] * unit, n = (size_t)(lo[i + 1] - lo[i]) * unit;
         FBF_CUDA(cudaMemcpyAsync(d_in + off, img + off, n * sizeof(float), cudaMemcpyHostToDevice, si), "H2D");
+        mark("in", si);
         if ((rc = ctx->event(2 * i, &ev)) != FBF_OK) return rc;
         FBF_CUDA(cudaEventRecord(ev, si), "event");
     }
@@ -457,17 +470,31 @@ int filter_frames_on_device(int dev, const float* img, int n_frames, int width, 
                               (long long)fp, width, height, lo[i + 1] - lo[i], 0, height};
         float2* sp = d_scr ? d_scr + (size_t)lo[i] * unit : nullptr;
         // intensity validation runs inside the kernel (every pixel is combined once)
+        mark("k0", sc);
         rc = run_job(*ctx, job, theta, a, border, sp, ctx->d_counters, sc, d_flag);
         if (rc != FBF_OK) return rc;
+        mark("k1", sc);
         if ((rc = ctx->event(2 * i + 1, &ev)) != FBF_OK) return rc;
         FBF_CUDA(cudaEventRecord(ev, sc), "event");
         FBF_CUDA(cudaStreamWaitEvent(so, ev, 0), "wait");
         const size_t off = (size_t)lo[i] * unit, n = (size_t)(lo[i + 1] - lo[i]) * unit;
         FBF_CUDA(cudaMemcpyAsync(out + off, d_out + off, n * sizeof(float), cudaMemcpyDeviceToHost, so), "D2H");
+        mark("out", so);
     }
     FBF_CUDA(cudaMemcpyAsync(ctx->h_counters, ctx->d_counters, 2 * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, so), "D2H counters");
     FBF_CUDA(cudaStreamSynchronize(so), "filter");
+    if (trace) {
+        cudaDeviceSynchronize();
+        std::string line = "fbf trace (us):";
+        for (auto& [what, e] : tl) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, tl[0].second, e);
+            line += std::string(" ") + what + "=" + std::to_string((int)(ms * 1000.f));
+        }
+        for (auto& [what, e] : tl) cudaEventDestroy(e);
+        std::fprintf(stderr, "%s\n", line.c_str());
+    }
     if (ctx->h_counters[1]) return fail(FBF_ERANGE, "filter: pixel intensity outside [0, R]");
     if (fallbacks) *fallbacks += (long long)ctx->h_counters[0];
     return FBF_OK;
