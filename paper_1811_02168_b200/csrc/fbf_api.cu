@@ -270,22 +270,26 @@ Plan make_plan(int K, int r) {
                                  {8, P, 1, 1}, {8, S, 1, 1}, {16, P, 1, 1}};
     Plan best;
     double best_bal = -1.0;
-    for (const Pref& pf : prefs) {
-        const fbf_dev::QEntry* qe = pf.mode == S ? &ent.split8 : pf.q == 16 ? &ent.pair16 : &ent.pair8;
-        if (!qe->launch[0] || (fq && fq != pf.q) || (fmode >= 0 && fmode != pf.mode) || (fngb && fngb != pf.ngb) ||
-            (fncb && fncb != pf.ncb))
-            continue;
-        const int mp = qe->max_pairs[pf.ngb][pf.ncb];
-        if (mp < 2) continue;
-        auto chunks = split_chunks(K, mp);
-        double bal = 1.0;
-        for (const Chunk& c : chunks)
-            bal = std::min(bal, subpartition_balance((pf.mode == S ? 2 : 1) * c.n_pairs));
-        const bool better = best_bal < 0 || chunks.size() < best.chunks.size() ||
-                            (chunks.size() == best.chunks.size() && bal > best_bal + 1e-9);
-        if (better) {
-            best = Plan{std::move(chunks), pf.q, pf.mode, pf.ngb, pf.ncb, qe};
-            best_bal = bal;
+    // overrides first; a radius without a matching variant takes the free choice
+    for (int forced = 1; forced >= 0 && !best.ent; --forced) {
+        for (const Pref& pf : prefs) {
+            const fbf_dev::QEntry* qe = pf.mode == S ? &ent.split8 : pf.q == 16 ? &ent.pair16 : &ent.pair8;
+            if (!qe->launch[0]) continue;
+            if (forced && ((fq && fq != pf.q) || (fmode >= 0 && fmode != pf.mode) || (fngb && fngb != pf.ngb) ||
+                           (fncb && fncb != pf.ncb)))
+                continue;
+            const int mp = qe->max_pairs[pf.ngb][pf.ncb];
+            if (mp < 2) continue;
+            auto chunks = split_chunks(K, mp);
+            double bal = 1.0;
+            for (const Chunk& c : chunks)
+                bal = std::min(bal, subpartition_balance((pf.mode == S ? 2 : 1) * c.n_pairs));
+            const bool better = best_bal < 0 || chunks.size() < best.chunks.size() ||
+                                (chunks.size() == best.chunks.size() && bal > best_bal + 1e-9);
+            if (better) {
+                best = Plan{std::move(chunks), pf.q, pf.mode, pf.ngb, pf.ncb, qe};
+                best_bal = bal;
+            }
         }
     }
     return best;
