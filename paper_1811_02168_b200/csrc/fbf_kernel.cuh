@@ -470,14 +470,17 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
     // compile-time offset XOFF), the gen offset, and the row q (-1: no item).
     constexpr int XOFF = ((-R) % 4 + 4) % 4;
     struct GenItem {
-        int fso, go, q, xl;
+        int fso, go, q, cm;  // cm: bit 0/1 = pixel a/b lies in the image (or the border is not zero)
     };
-    auto gen_items = [&](GenItem (&gi)[GITER]) {
+    auto gen_items = [&](const Segment& sg, GenItem (&gi)[GITER]) {
+        const bool zb = p.border == 2;
 #pragma unroll
         for (int it = 0; it < GITER; ++it) {
             const int item = it * kGenThreads + tid;
             const int q = item / HGW, xl = 2 * (item - q * HGW);
-            gi[it] = GenItem{q * FSW + xl + XOFF, q * GS + xl, item < Q * HGW ? q : -1, xl};
+            const int gx = sg.x0 - R + xl;
+            const int cm = (!zb || (gx >= 0 && gx < p.width) ? 1 : 0) | (!zb || (gx + 1 >= 0 && gx + 1 < p.width) ? 2 : 0);
+            gi[it] = GenItem{q * FSW + xl + XOFF, q * GS + xl, item < Q * HGW ? q : -1, cm};
         }
     };
     auto gen_step = [&](const Segment& sg, int s, int fb, int gb, const GenItem (&gi)[GITER]) {
@@ -486,22 +489,22 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
         float2* gbuf = gen + gb * np * Q * GS;
         // rows of the step that feed an output row and (zero border) lie in the image
         int lo = max(a, sg.ya - R), hi = min(a + Q, sg.yb + R);
-        const bool zb = p.border == 2;
-        if (zb) {
+        if (p.border == 2) {
             lo = max(lo, 0);
             hi = min(hi, p.height);
         }
+        const unsigned nrows = (unsigned)max(hi - lo, 0);
         const float inv = p.inv_period;
-        const int gx0 = sg.x0 - R;
+        const bool kfirst = p.k_first > 1;
 #pragma unroll 2
         for (int it = 0; it < GITER; ++it) {
             const int q = gi[it].q;
             if (q >= 0) {
-                const bool rowok = a + q >= lo && a + q < hi;
-                const int gx = gx0 + gi[it].xl;
-                const bool va = rowok && (!zb || (gx >= 0 && gx < p.width));
-                const bool vb = rowok && (!zb || (gx + 1 >= 0 && gx + 1 < p.width));
-                const float2 f = make_float2(va ? fs[gi[it].fso] : 0.f, vb ? fs[gi[it].fso + 1] : 0.f);
+                // unconditional loads (rows the loader skipped hold stale values), then select
+                const float fa = fs[gi[it].fso], fbv = fs[gi[it].fso + 1];
+                const bool rowok = (unsigned)(a + q - lo) < nrows;
+                const bool va = rowok && (gi[it].cm & 1), vb = rowok && (gi[it].cm & 2);
+                const float2 f = make_float2(va ? fa : 0.f, vb ? fbv : 0.f);
                 // per pixel (first, second) channel pairs, stored as float2 at gp[0] / gp[1]
                 float2* gp = gbuf + gi[it].go;
                 if (zk) {
@@ -511,8 +514,8 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                 if (NKR > 0) {
                     const CS2 h = harmonic1x2(f, inv);
                     const float2 w0 = make_float2(h.c.x, h.s.x), w1 = make_float2(h.c.y, h.s.y);
-                    float2 z0 = p.k_first > 1 ? harmonic_first1(w0, p.k_first) : w0;
-                    float2 z1 = p.k_first > 1 ? harmonic_first1(w1, p.k_first) : w1;
+                    float2 z0 = kfirst ? harmonic_first1(w0, p.k_first) : w0;
+                    float2 z1 = kfirst ? harmonic_first1(w1, p.k_first) : w1;
                     if (!va) z0 = make_float2(0.f, 0.f);
                     if (!vb) z1 = make_float2(0.f, 0.f);
                     float2* gk = gp + zk * (Q * GS);
@@ -577,6 +580,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
     };
     auto combine_step = [&](const Segment& sg, int cb, CombItem (&ci)[CITER], const float2 (&fv)[CITER]) {
         const float* cbase = reinterpret_cast<const float*>(colout + cb * np * Q * kTW);
+        const bool kfirst_c = p.k_first > 1;
 #pragma unroll
         for (int it = 0; it < CITER; ++it) {
             CombItem& c = ci[it];
@@ -595,25 +599,32 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                 // planar column results [pair][channel][q][TW]: float2 = the two pixels of one channel
                 const float2* go = reinterpret_cast<const float2*>(cbase + c.co);
                 constexpr int CSTR = Q * kTW / 2;  // float2 per channel plane
-                if (zk) {
-                    const float2 c0 = make_float2(p.coeff[0], p.coeff[0]);
-                    num = __ffma2_rn(c0, go[0], num);
-                    den = __ffma2_rn(c0, go[CSTR], den);
-                }
-                if (NKR > 0) {
-                    const CS2 c1 = harmonic1x2(f, p.inv_period);
-                    CS2 cs = p.k_first > 1 ? harmonic_first2(c1, p.k_first) : c1;
-                    const float2* gk = go + zk * 2 * CSTR;
-#pragma unroll
-                    for (int kk = 0; kk < NKR; ++kk) {
-                        const float2 ck = make_float2(p.coeff[zk + kk], p.coeff[zk + kk]);
-                        const float2* pn = gk + (4 * kk) * CSTR;  // G(C_k f), G(S_k f)
-                        const float2* pd = pn + 2 * CSTR;         // G(C_k), G(S_k)
-                        num = __ffma2_rn(ck, __ffma2_rn(cs.s, pn[CSTR], __fmul2_rn(cs.c, pn[0])), num);
-                        den = __ffma2_rn(ck, __ffma2_rn(cs.s, pd[CSTR], __fmul2_rn(cs.c, pd[0])), den);
-                        if (kk + 1 < NKR) cs = rotate2(cs, c1);
+                // ZK (chunk holds k = 0) as a compile-time constant: coefficient and
+                // column-tile offsets become immediates
+                auto accumulate = [&](auto zkc) {
+                    constexpr int ZK = decltype(zkc)::value;
+                    if (ZK) {
+                        const float2 c0 = make_float2(p.coeff[0], p.coeff[0]);
+                        num = __ffma2_rn(c0, go[0], num);
+                        den = __ffma2_rn(c0, go[CSTR], den);
                     }
-                }
+                    if (NKR > 0) {
+                        const CS2 c1 = harmonic1x2(f, p.inv_period);
+                        CS2 cs = kfirst_c ? harmonic_first2(c1, p.k_first) : c1;
+                        const float2* gk = go + ZK * 2 * CSTR;
+#pragma unroll
+                        for (int kk = 0; kk < NKR; ++kk) {
+                            const float2 ck = make_float2(p.coeff[ZK + kk], p.coeff[ZK + kk]);
+                            const float2* pn = gk + (4 * kk) * CSTR;  // G(C_k f), G(S_k f)
+                            const float2* pd = pn + 2 * CSTR;         // G(C_k), G(S_k)
+                            num = __ffma2_rn(ck, __ffma2_rn(cs.s, pn[CSTR], __fmul2_rn(cs.c, pn[0])), num);
+                            den = __ffma2_rn(ck, __ffma2_rn(cs.s, pd[CSTR], __fmul2_rn(cs.c, pd[0])), den);
+                            if (kk + 1 < NKR) cs = rotate2(cs, c1);
+                        }
+                    }
+                };
+                if (zk) accumulate(std::integral_constant<int, 1>{});
+                else accumulate(std::integral_constant<int, 0>{});
                 if (p.last_chunk) {
                     float oa = f.x, ob = f.y;
                     unsigned nfb = 0;
@@ -731,7 +742,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
         } else if (role == kRoleGen) {
             // ============================= GEN ==============================
             GenItem gi[GITER];
-            gen_items(gi);
+            gen_items(sg, gi);
             for (int t = 0; t < steps; ++t) {
                 const int g = gstep + t;
                 const int fb = g % NFS, gb = g % ngb;

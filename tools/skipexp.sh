@@ -1,2 +1,2 @@
-FBF_STREAM_BANDS=8 timeout 60 python tools/stream_check.py c1
-for nb in 8 16; do FBF_TRACE=1 FBF_STREAM_BANDS=$nb timeout 60 python tools/e2e_probe.py 2>&1 | tail -2; done
+timeout 300 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+for c in c1 c3 c4 c2 c0; do timeout 120 python tools/kbench.py --config $c --iters 30 --tag "comb-v2"; done
