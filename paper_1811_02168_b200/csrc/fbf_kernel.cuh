@@ -69,10 +69,19 @@ constexpr size_t kSmemReservedPerBlock = 1024;
 //   kSplitMode: one ROW and one COL warp per pair, connected by a ring of row
 //               blocks -- twice the warps, so the FFMA2 work spreads more evenly
 //               over the four SM sub-partitions (warp id mod 4).
-constexpr int kPairMode = 0, kSplitMode = 1;
-// threads of a launch: FFMA2 warps, plus combine, gen and loader
+//   kHalfMode : one ROW warp and two COL warps per pair; COL warp h produces
+//               the output rows of parity h with R (not 2R) partial sums and
+//               half the taps per row (same per-output order, same bits). The
+//               3 np FFMA2 warps have weights 2:1:1, which the host places on
+//               the sub-partitions so that each gets the same FFMA2 work
+//               (Params::warp_role), for up to 7 pairs per launch.
+constexpr int kPairMode = 0, kSplitMode = 1, kHalfMode = 2;
+constexpr int kHalfMaxPairs = 7;
+// threads of a launch: FFMA2 warps, plus combine, gen and loader (half mode:
+// rounded up to whole sub-partition rows, unused slots idle)
 __host__ __device__ constexpr int block_threads(int pairs, int mode) {
-    return (mode == kPairMode ? 1 : 2) * 32 * pairs + kExtraThreads;
+    return mode == kHalfMode ? 4 * ((3 * pairs + 9 + 3) / 4) * 32
+                             : (mode == kPairMode ? 1 : 2) * 32 * pairs + kExtraThreads;
 }
 enum Role { kRoleGen = 0, kRoleRow = 1, kRoleCol = 2, kRoleLoad = 3, kRoleComb = 4, kRoleIdle = 5 };
 
@@ -109,6 +118,8 @@ struct Params {
     float coeff[kMaxKR + 1];     // c_k of the chunk, ascending k
     float inv_period;            // 1 / (2T + 1)
     unsigned long long* prof;    // dev builds with FBF_PHASES: per warp slot [total, wait A, wait B, CTAs] cycles
+    unsigned char warp_role[32]; // half mode: Role and role index of every warp slot
+    unsigned char warp_idx[32];
 };
 
 #ifdef FBF_PHASES
@@ -140,7 +151,7 @@ struct Geometry {
     // live in registers ("scatter": every row-pass output is read once), so the
     // ring is just a double buffer of Q rows; larger radii gather a window of
     // ring rows (RB blocks) per step.
-    static constexpr bool SCATTER = R <= 16;
+    static constexpr bool SCATTER = R <= 16 || M == kHalfMode;
     static_assert(SCATTER || !PAIR, "pair mode keeps the column partial sums in registers");
     static constexpr int RB = 1 + (2 * R + Q - 1) / Q;           // ring blocks a gather column pass reads
     static constexpr int RBN = SCATTER ? 1 : RB;                 // blocks a column pass reads
@@ -378,6 +389,41 @@ __device__ __forceinline__ void col_scatter(const float2* __restrict__ hin, floa
     }
 }
 
+// Half of the scatter column pass: output rows q of the step with q % 2 == H
+// (q = r: the output completed by input row r). st[i] holds the partial sum of
+// the i-th pending output of this parity: R of them. A completing row (r % 2 ==
+// H) finishes st[0], shifts, and opens the output R rows below; the other rows
+// add to all R pending outputs. Per output, contributions still enter in
+// ascending input row from a product, so the bits equal col_scatter's.
+template <int R, int Q, int H>
+__device__ __forceinline__ void col_scatter_half(const float2* __restrict__ hin, float2 (&st)[R], float* out,
+                                                 bool store, const Params& pp) {
+    constexpr int RS = kTW + 2;
+#pragma unroll
+    for (int r = 0; r < Q; ++r) {
+        const float2 v = hin[r * RS];
+        if ((r & 1) == H) {
+            const float2 o = ffma2(v, pp.taps_col[R], st[0]);
+#pragma unroll
+            for (int i = 0; i + 1 < R; ++i) {
+                const int d = R - 2 * (i + 1);
+                st[i] = ffma2(v, pp.taps_col[d >= 0 ? d : -d], st[i + 1]);
+            }
+            st[R - 1] = __fmul2_rn(v, make_float2(pp.taps_col[R], pp.taps_col[R]));
+            if (store) {  // planar: [channel][q][TW]
+                out[r * kTW] = o.x;
+                out[(Q + r) * kTW] = o.y;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                const int d = R - 1 - 2 * i;
+                st[i] = ffma2(v, pp.taps_col[d >= 0 ? d : -d], st[i]);
+            }
+        }
+    }
+}
+
 // Per-segment geometry shared by every role.
 struct Segment {
     int frame, x0, ya, yb, a0, steps;
@@ -402,10 +448,14 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
     float2* colout = gen + (size_t)ngb * np * Q * GS;                    // [ncb][np] x [2][Q][TW] floats
     float2* ring = colout + (size_t)ncb * np * Q * kTW;                  // [np][RROWS][RS]
 
-    const int nrole = np * 32;  // threads of each of the ROW/PAIR and COL roles
+    const int nrole = np * 32;  // threads of the ROW/PAIR role (and of the COL role in split mode)
     const int nf = G::PAIR ? nrole : 2 * nrole;  // FFMA2 threads
     int role, tid;  // Role; ROW is PAIR in pair mode
-    {
+    if constexpr (M == kHalfMode) {
+        const int w = (int)(threadIdx.x / 32);
+        role = p.warp_role[w];
+        tid = p.warp_idx[w] * 32 + (int)(threadIdx.x & 31);
+    } else {
         // Roles are numbered from the LAST warp down: the FFMA2 warps get the highest
         // warp ids, which the issue arbiter of a sub-partition serves first; the
         // latency-bound roles (gen, combine, loader) have slack and fill the gaps.
@@ -421,7 +471,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
     const int zk = p.k_lo == 0 ? 1 : 0;  // k = 0 contributes the single pair (f, 1)
     // named-barrier thread counts: producers + consumers of each handoff
     const int gen_threads = kGenThreads + nrole;   // GEN -> ROW/PAIR and back
-    const int col_threads = nrole + kCombThreads;  // COL/PAIR -> COMB and back
+    const int col_threads = (M == kHalfMode ? 2 : 1) * nrole + kCombThreads;  // COL/PAIR -> COMB and back
     constexpr int kFsThreads = kGenThreads + 32;   // GEN -> LOAD (f stage empty)
 #ifdef FBF_PHASES
     long long _pw[2] = {0, 0};
@@ -430,7 +480,10 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
     unsigned n_fallbacks = 0;  // combine threads: fallback pixels (filter.cpp:203-208)
     if (threadIdx.x == 0) {
         for (int b = 0; b < NFS; ++b) mbar_init(&fs_full[b], 1);
-        for (int b = 0; b < np * RBP; ++b) { mbar_init(&ring_full[b], 1); mbar_init(&ring_empty[b], 1); }
+        for (int b = 0; b < np * RBP; ++b) {
+            mbar_init(&ring_full[b], 1);
+            mbar_init(&ring_empty[b], M == kHalfMode ? 2 : 1);  // both COL halves release a block
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -823,6 +876,25 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
             const int pr = tid / 32;
             const float2* myring = ring + (size_t)pr * RROWS * RS;
             if constexpr (!FMA || G::PAIR) {
+            } else if constexpr (M == kHalfMode) {
+                const int pr = tid / 64, h = (tid / 32) & 1;  // pair, output-row parity
+                const float2* hring = ring + (size_t)pr * RROWS * RS;
+                float2 st[R];
+#pragma unroll
+                for (int i = 0; i < R; ++i) st[i] = make_float2(0.f, 0.f);  // new segment
+                for (int t = 0; t < steps; ++t) {
+                    const int g = gstep + t;
+                    const int blk = g % RBP, cb = g % ncb;
+                    PWAIT(0, &ring_full[pr * RBP + blk], (unsigned)((g / RBP) & 1));
+                    if (g >= ncb) PSYNC(1, kBarColEmpty + cb, col_threads);
+                    float* oc = reinterpret_cast<float*>(colout + ((size_t)cb * np + pr) * Q * kTW) + lane;
+                    const float2* hin = hring + (size_t)blk * Q * RS + lane;
+                    if (h == 0) col_scatter_half<R, Q, 0>(hin, st, oc, t >= s0, p);
+                    else col_scatter_half<R, Q, 1>(hin, st, oc, t >= s0, p);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&ring_empty[pr * RBP + blk]);  // block free for row pass g + RBP
+                    named_arrive(kBarColFull + cb, col_threads);
+                }
             } else if constexpr (G::SCATTER) {
                 float2 st[2 * R];
 #pragma unroll
@@ -869,7 +941,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
         gstep += steps;
     }
     };  // run_roles
-    run_roles(std::true_type{});
+    if (role != kRoleIdle) run_roles(std::true_type{});
     if (role == kRoleComb && p.fallbacks) {
         const unsigned w = __reduce_add_sync(0xffffffffu, n_fallbacks);
         if (lane == 0 && w) atomicAdd(p.fallbacks, (unsigned long long)w);

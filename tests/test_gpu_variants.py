@@ -25,6 +25,8 @@ VARIANTS = {
     "split_q8": {"FBF_MODE": "1", "FBF_Q": "8"},
     "pair_q8_single_buffers": {"FBF_MODE": "0", "FBF_Q": "8", "FBF_NGB": "1", "FBF_NCB": "1"},
     "split_q8_single_buffers": {"FBF_MODE": "1", "FBF_Q": "8", "FBF_NGB": "1", "FBF_NCB": "1"},
+    "half_q8": {"FBF_MODE": "2", "FBF_Q": "8"},
+    "half_q8_single_buffers": {"FBF_MODE": "2", "FBF_Q": "8", "FBF_NGB": "1", "FBF_NCB": "1"},
     "bulk_staging": {"FBF_STAGE": "bulk"},
 }
 

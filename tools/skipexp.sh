@@ -1,2 +1,3 @@
-timeout 300 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-for c in c1 c3 c4 c2 c0; do timeout 120 python tools/kbench.py --config $c --iters 30 --tag "comb-v2"; done
+timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+for c in c1 c3 c4 c2 c0; do timeout 120 python tools/kbench.py --config $c --iters 30 --tag "default"; done
+for c in c2 c3; do FBF_MODE=2 timeout 120 python tools/kbench.py --config $c --iters 20 --tag "half"; done
