@@ -50,5 +50,5 @@ nw = nf + 9
 for w in range(32):
     tot, wa, wb, n = buf[4 * w:4 * w + 4]
     if n == 0: continue
-    nm = placed_name(w, np_) if mode == 2 else names[nw - 1 - w]
+    nm = names[nw - 1 - w] if mode != 2 else "slot"
     print(f"warp {w:2d} smsp {w % 4} {nm:6s} cycles/CTA {tot / n:10.0f}  waitA {wa / tot * 100:5.1f}%  waitB {wb / tot * 100:5.1f}%  busy {100 - (wa + wb) / tot * 100:5.1f}%")
