@@ -159,7 +159,7 @@ struct Geometry {
     // row pass of the next step starts after its column pass, one block suffices
     static constexpr int RBP = PAIR ? 1 : RBN + 1;
     static constexpr int RROWS = RBP * Q;                        // ring rows per pair
-    static constexpr int RS = kTW + 2;                           // ring stride (float2), RS/2 odd
+    static constexpr int RS = kTW + 1;                           // ring stride (float2), odd: conflict-free STS.64 across rows
     static constexpr int NFS = 3;                                // f staging buffers (loader runs ahead)
     static constexpr int kMaxBuf = 2;                            // gen / column buffers (named barrier ids)
     static constexpr size_t fstage_bytes = sizeof(float) * NFS * Q * FSW;  // multiple of 128
@@ -305,7 +305,7 @@ __device__ __forceinline__ void tma_bulk_g2s(float* smem_dst, const float* gsrc,
 // columns); Q outputs per lane from (Q+2R)/2 LDS.128 of gen row q. Arrives on
 // `gen_empty` once the gen rows are read, then writes the ring block.
 template <int R, int Q>
-__device__ __forceinline__ void row_pass(const float4* __restrict__ gin, float4* __restrict__ hout, const Params& pp,
+__device__ __forceinline__ void row_pass(const float4* __restrict__ gin, float2* __restrict__ hout, const Params& pp,
                                          int gen_empty_id, int gen_threads) {
     float2 acc[Q];
 #pragma unroll
@@ -326,8 +326,7 @@ __device__ __forceinline__ void row_pass(const float4* __restrict__ gin, float4*
     }
     named_arrive(gen_empty_id, gen_threads);  // this warp's gen rows consumed
 #pragma unroll
-    for (int o = 0; o < Q / 2; ++o)
-        hout[o] = make_float4(acc[2 * o].x, acc[2 * o].y, acc[2 * o + 1].x, acc[2 * o + 1].y);
+    for (int o = 0; o < Q; ++o) hout[o] = acc[o];  // STS.64 straight from the accumulator pairs
 }
 
 // Vertical pass of ring block `blk` (the step's Q rows): lane = column, Q
@@ -371,7 +370,7 @@ __device__ __forceinline__ void col_pass(const float2* __restrict__ ring_pair, i
 template <int R, int Q>
 __device__ __forceinline__ void col_scatter(const float2* __restrict__ hin, float2 (&st)[2 * R], float* out, bool store,
                                             const Params& pp) {
-    constexpr int RS = kTW + 2;
+    constexpr int RS = kTW + 1;
 #pragma unroll
     for (int r = 0; r < Q; ++r) {
         const float2 v = hin[r * RS];
@@ -398,7 +397,7 @@ __device__ __forceinline__ void col_scatter(const float2* __restrict__ hin, floa
 template <int R, int Q, int H>
 __device__ __forceinline__ void col_scatter_half(const float2* __restrict__ hin, float2 (&st)[R], float* out,
                                                  bool store, const Params& pp) {
-    constexpr int RS = kTW + 2;
+    constexpr int RS = kTW + 1;
 #pragma unroll
     for (int r = 0; r < Q; ++r) {
         const float2 v = hin[r * RS];
@@ -438,7 +437,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
     constexpr int GW = G::GW, GS = G::GS, FSW = G::FSW, RB = G::RB, RBP = G::RBP, RROWS = G::RROWS, RS = G::RS;
     constexpr int NFS = G::NFS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int np = p.n_pairs, ngb = p.ngb, ncb = p.ncb;
+    const int np = p.n_pairs, ngb = p.ngb, ncb = p.ncb;  // ngb, ncb in {1, 2}: buffer index = g & (n - 1)
     float* fstage = reinterpret_cast<float*>(smem_raw);                         // [NFS][Q][FSW]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + G::fstage_bytes);
     uint64_t* fs_full = bars;                                // [NFS] LOAD -> GEN (cp.async completion)
@@ -798,7 +797,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
             gen_items(sg, gi);
             for (int t = 0; t < steps; ++t) {
                 const int g = gstep + t;
-                const int fb = g % NFS, gb = g % ngb;
+                const int fb = g % NFS, gb = (g & (ngb - 1));
                 PWAIT(0, &fs_full[fb], (unsigned)((g / NFS) & 1));
                 if (g >= ngb) PSYNC(1, kBarGenEmpty + gb, gen_threads);
 #ifndef FBF_SKIP_GEN
@@ -814,7 +813,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
             comb_items(sg, ci);
             for (int t = 0; t < steps; ++t) {
                 const int g = gstep + t;
-                const int cb = g % ncb;
+                const int cb = (g & (ncb - 1));
                 float2 fv[CITER];
                 if (t >= s0) combine_load(sg, ci, fv);
                 PSYNC(0, kBarColFull + cb, col_threads);
@@ -836,11 +835,11 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                 for (int i = 0; i < 2 * R; ++i) st[i] = make_float2(0.f, 0.f);  // new segment
                 for (int t = 0; t < steps; ++t) {
                     const int g = gstep + t;
-                    const int gb = g % ngb, cb = g % ncb;
+                    const int gb = (g & (ngb - 1)), cb = (g & (ncb - 1));
                     PSYNC(0, kBarGenFull + gb, gen_threads);
                     const float4* gin =
                         reinterpret_cast<const float4*>(gen + (((size_t)gb * np + pr) * Q + q) * GS + xc * Q);
-                    row_pass<R, Q>(gin, reinterpret_cast<float4*>(hbuf + (size_t)q * RS + xc * Q), p,
+                    row_pass<R, Q>(gin, hbuf + (size_t)q * RS + xc * Q, p,
                                    kBarGenEmpty + gb, gen_threads);
                     __syncwarp();  // the step's row-pass block is complete
                     // column buffer cb must have been consumed by COMB even on warm-up steps:
@@ -860,12 +859,12 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                 float2* myring = ring + (size_t)pr * RROWS * RS;
                 for (int t = 0; t < steps; ++t) {
                     const int g = gstep + t;
-                    const int gb = g % ngb, blk = g % RBP;
+                    const int gb = (g & (ngb - 1)), blk = g % RBP;
                     PSYNC(0, kBarGenFull + gb, gen_threads);
                     // ring block blk last held step g - RBP, read up to column pass g - RBP + RBN - 1
                     if (g >= RBP) PWAIT(1, &ring_empty[pr * RBP + blk], (unsigned)((g / RBP - 1) & 1));
                     const float4* gin = reinterpret_cast<const float4*>(gen + (((size_t)gb * np + pr) * Q + q) * GS + xc * Q);
-                    float4* hout = reinterpret_cast<float4*>(myring + ((size_t)blk * Q + q) * RS + xc * Q);
+                    float2* hout = myring + ((size_t)blk * Q + q) * RS + xc * Q;
                     row_pass<R, Q>(gin, hout, p, kBarGenEmpty + gb, gen_threads);
                     __syncwarp();  // ring block complete
                     if (lane == 0) mbar_arrive(&ring_full[pr * RBP + blk]);
@@ -884,7 +883,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                 for (int i = 0; i < R; ++i) st[i] = make_float2(0.f, 0.f);  // new segment
                 for (int t = 0; t < steps; ++t) {
                     const int g = gstep + t;
-                    const int blk = g % RBP, cb = g % ncb;
+                    const int blk = g % RBP, cb = (g & (ncb - 1));
                     PWAIT(0, &ring_full[pr * RBP + blk], (unsigned)((g / RBP) & 1));
                     if (g >= ncb) PSYNC(1, kBarColEmpty + cb, col_threads);
                     float* oc = reinterpret_cast<float*>(colout + ((size_t)cb * np + pr) * Q * kTW) + lane;
@@ -901,7 +900,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                 for (int i = 0; i < 2 * R; ++i) st[i] = make_float2(0.f, 0.f);  // new segment
                 for (int t = 0; t < steps; ++t) {
                     const int g = gstep + t;
-                    const int blk = g % RBP, cb = g % ncb;
+                    const int blk = g % RBP, cb = (g & (ncb - 1));
                     PWAIT(0, &ring_full[pr * RBP + blk], (unsigned)((g / RBP) & 1));
                     // column buffer cb must have been consumed by COMB even on warm-up steps:
                     // the arrival below completes a phase of col_full[cb]
@@ -915,7 +914,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
             } else {
                 for (int t = 0; t < steps; ++t) {
                     const int g = gstep + t;
-                    const int blk = g % RBP, cb = g % ncb;
+                    const int blk = g % RBP, cb = (g & (ncb - 1));
                     const bool do_col = t >= s0;
                     PWAIT(0, &ring_full[pr * RBP + blk], (unsigned)((g / RBP) & 1));
                     float2 acc[Q];
