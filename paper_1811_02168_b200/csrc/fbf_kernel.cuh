@@ -233,6 +233,14 @@ __device__ __forceinline__ float2 harmonic_first1(float2 w, int k_first) {
     return z;
 }
 
+// 1/x to ~1 ulp (MUFU.RCP); out = num / den has the same tolerance budget as
+// __fdividef without its denormal-range fix-up instructions (den > 1e-12 here)
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 __device__ __forceinline__ float2 ffma2(float2 a, float w, float2 c) {
     return __ffma2_rn(a, make_float2(w, w), c);
 }
@@ -630,6 +638,9 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
             if (ci[it].y < sg.yb && ci[it].colok) fv[it] = make_float2(__ldg(ci[it].sp), ci[it].vb ? __ldg(ci[it].sp + 1) : 0.f);
         }
     };
+    // per-step pointer advances (64-bit adds, no wide multiplies in the step loop)
+    const long long src_step = (long long)Q * p.src_pitch, dst_step = (long long)Q * p.dst_pitch,
+                    acc_step = (long long)Q * p.width;
     auto combine_step = [&](const Segment& sg, int cb, CombItem (&ci)[CITER], const float2 (&fv)[CITER]) {
         const float* cbase = reinterpret_cast<const float*>(colout + cb * np * Q * kTW);
         const bool kfirst_c = p.k_first > 1;
@@ -680,8 +691,8 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                 if (p.last_chunk) {
                     float oa = f.x, ob = f.y;
                     unsigned nfb = 0;
-                    if (den.x > 1e-12f) oa = __fdividef(num.x, den.x); else ++nfb;
-                    if (den.y > 1e-12f) ob = __fdividef(num.y, den.y); else nfb += vb;
+                    if (den.x > 1e-12f) oa = num.x * rcp_approx(den.x); else ++nfb;
+                    if (den.y > 1e-12f) ob = num.y * rcp_approx(den.y); else nfb += vb;
                     n_fallbacks += nfb;
                     c.dp[0] = oa;
                     if (vb) c.dp[1] = ob;
@@ -691,9 +702,9 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                 }
             }
             c.y += Q;
-            c.sp += (long long)Q * p.src_pitch;
-            c.dp += (long long)Q * p.dst_pitch;
-            if (c.ap) c.ap += (long long)Q * p.width;
+            c.sp += src_step;
+            c.dp += dst_step;
+            if (!p.first_chunk || !p.last_chunk) c.ap += acc_step;
         }
     };
 
