@@ -233,6 +233,15 @@ __device__ __forceinline__ float2 harmonic_first1(float2 w, int k_first) {
     return z;
 }
 
+// float2 store to shared memory as st.shared.v2.f32: a plain float2 store through
+// a generic pointer makes ptxas copy FMUL2/FFMA2 result pairs into a staging
+// pair first (two MOVs per store, measured in the gen loop)
+__device__ __forceinline__ void sts2(float2* p, float2 v) {
+    // volatile keeps the order against the (volatile) barrier instructions that
+    // publish the data; no memory clobber, so loads and math still schedule freely
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};\n" ::"r"((unsigned)__cvta_generic_to_shared(p)), "f"(v.x), "f"(v.y));
+}
+
 // 1/x to ~1 ulp (MUFU.RCP); out = num / den has the same tolerance budget as
 // __fdividef without its denormal-range fix-up instructions (den > 1e-12 here)
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -568,8 +577,8 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                 // per pixel (first, second) channel pairs, stored as float2 at gp[0] / gp[1]
                 float2* gp = gbuf + gi[it].go;
                 if (zk) {
-                    gp[0] = make_float2(f.x, va ? 1.f : 0.f);
-                    gp[1] = make_float2(f.y, vb ? 1.f : 0.f);
+                    sts2(gp, make_float2(f.x, va ? 1.f : 0.f));
+                    sts2(gp + 1, make_float2(f.y, vb ? 1.f : 0.f));
                 }
                 if (NKR > 0) {
                     const CS2 h = harmonic1x2(f, inv);
@@ -583,10 +592,10 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                     for (int kk = 0; kk < NKR; ++kk) {
                         float2* pf = gk + (2 * kk) * (Q * GS);      // (C_k f, S_k f)
                         float2* pc = gk + (2 * kk + 1) * (Q * GS);  // (C_k, S_k)
-                        pf[0] = __fmul2_rn(z0, make_float2(f.x, f.x));
-                        pf[1] = __fmul2_rn(z1, make_float2(f.y, f.y));
-                        pc[0] = z0;
-                        pc[1] = z1;
+                        sts2(pf, __fmul2_rn(z0, make_float2(f.x, f.x)));
+                        sts2(pf + 1, __fmul2_rn(z1, make_float2(f.y, f.y)));
+                        sts2(pc, z0);
+                        sts2(pc + 1, z1);
                         if (kk + 1 < NKR) {
                             z0 = rotate1(z0, w0);
                             z1 = rotate1(z1, w1);
