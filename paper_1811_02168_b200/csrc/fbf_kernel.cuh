@@ -53,9 +53,15 @@ constexpr int kMaxKR = 4;        // k >= 1 terms per launch (template parameter 
 constexpr int kMaxPairs = 1 + 2 * kMaxKR;
 constexpr int kMaxRadius = 32;
 constexpr int kQ16MaxRadius = 16;  // Q = 16 steps are instantiated for r <= 16
-constexpr int kCombWarps = 4;
+#ifndef FBF_COMB_WARPS
+#define FBF_COMB_WARPS 4
+#endif
+constexpr int kCombWarps = FBF_COMB_WARPS;
 constexpr int kCombThreads = kCombWarps * 32;
-constexpr int kGenWarps = 4;
+#ifndef FBF_GEN_WARPS
+#define FBF_GEN_WARPS 4
+#endif
+constexpr int kGenWarps = FBF_GEN_WARPS;
 constexpr int kGenThreads = kGenWarps * 32;
 constexpr int kExtraThreads = kCombThreads + kGenThreads + 32;  // combine + gen + loader
 constexpr size_t kSmemLimit = 232448;          // 227 KB opt-in per block on sm_100
@@ -821,6 +827,9 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                 PWAIT(0, &fs_full[fb], (unsigned)((g / NFS) & 1));
                 if (g >= ngb) PSYNC(1, kBarGenEmpty + gb, gen_threads);
 #ifndef FBF_SKIP_GEN
+#ifdef FBF_DEV_LIGHT_W0  // dev: only the light warps on the lone-pair sub-partition work
+                if (tid < 32)
+#endif
                 gen_step(sg, t, fb, gb, gi);
 #endif
                 // this warp's part of gen buffer gb written, fstage fb read
@@ -838,6 +847,9 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                 if (t >= s0) combine_load(sg, ci, fv);
                 PSYNC(0, kBarColFull + cb, col_threads);
 #ifndef FBF_SKIP_COMB
+#ifdef FBF_DEV_LIGHT_W0
+                if (tid < 32)
+#endif
                 if (t >= s0) combine_step(sg, cb, ci, fv);
 #endif
                 named_arrive(kBarColEmpty + cb, col_threads);  // this warp is done with column buffer cb
