@@ -1,2 +1,2 @@
-for lib in c2 g3 g3c2; do FBF_LIB=devlib/$lib.so timeout 120 python tools/kbench.py --config c1 --tag "$lib"; done
-timeout 120 python tools/kbench.py --config c1 --tag "base"
+timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+for c in c1 c3 c4 c2 c0; do timeout 120 python tools/kbench.py --config $c --iters 30 --tag "v22"; done
