@@ -95,6 +95,30 @@ int fbf_select_params(int kind, double sigma, int R, double eps, int K, int T, i
                       int threads, int* K_out, int* T_out, double* coeffs, int coeff_cap,
                       double* err_out);
 
+/* ---- L2 on the GPU: the period scan of approx.cpp:119-144 --------------- */
+/* errors[(K - K_lo) * t_max + T - 1] = E(K, T) = ||A c - b||^2 for the nK
+ * orders K_lo..K_lo+nK-1 and T = 1..t_max, FP64 on device `device`, one CTA
+ * per (K, T) (fbf_scan.cu). Agrees with fbf_scan_period_errors to ~1e-15
+ * relative near the minimum and ~1e-6 where A is ill-conditioned (tree
+ * reductions), not bit for bit. FBF_ECAPACITY above
+ * K = fbf_scan_gpu_max_order(R) (the design matrix lives in shared memory). */
+int fbf_scan_period_errors_gpu(const double* samples, int R, int K_lo, int nK, int t_max, int device,
+                               double* errors);
+int fbf_scan_gpu_max_order(int R);
+/* min_error_over_period (approx.cpp:132-144) through the GPU scan + exact
+ * host re-check: the same (T_best, E) as fbf_min_error_over_period. */
+int fbf_min_error_over_period_gpu(const double* samples, int R, int K, int t_max, int device, int* T_best,
+                                  double* err_out);
+/* fbf_optimize_parameters / fbf_select_params with the period scans on the
+ * GPU: every T whose GPU error lies within a relative 1e-4 of the GPU minimum
+ * is re-fitted with the host routine and the argmin of those exact errors is
+ * taken (smaller T on ties), so K, T, the coefficients and the error equal
+ * the host versions'. Orders above fbf_scan_gpu_max_order(R) scan on the host. */
+int fbf_optimize_parameters_gpu(const double* samples, int R, double tol, int t_max, int k_max, int device,
+                                int* K_out, int* T_out, double* coeffs, int coeff_cap, double* err_out,
+                                double* per_order, int* n_orders);
+int fbf_select_params_gpu(int kind, double sigma, int R, double eps, int K, int T, int method_fbf, int device,
+                          int* K_out, int* T_out, double* coeffs, int coeff_cap, double* err_out);
 /* ---- L3 filter: filter.cpp (the hot path, sm_100a) ---------------------- */
 /* fast_bilateral (filter.hpp:43-46, filter.cpp:129-213) on HOST buffers:
  * validates intensities, copies img to the device, runs the fused kernel,
@@ -138,10 +162,19 @@ int fbf_fast_bilateral_band_f32_device(const float* d_src, int src_row0, int src
  * [out_row0, out_row0 + out_rows) at radius ceil(3 theta). */
 int fbf_band_source_rows(int height, int out_row0, int out_rows, double theta, int border,
                          int* row0, int* rows);
+/* fast_bilateral on 8-bit host buffers (the CLI's PGM path: read_pgm,
+ * imageio.cpp:53-80, widens bytes exactly). Exactly one output: out_u8
+ * receives the result clamped to [0,255] and rounded half away from zero
+ * (write_clamped + write_pgm, tools/fourierbf.cpp:71-76, imageio.cpp:83-89);
+ * out_f32 the float result. 1 byte per pixel crosses PCIe each way instead of 4. */
+int fbf_fast_bilateral_u8(const unsigned char* img, int width, int height, double theta, int K, int T, int R,
+                          const double* coeffs, int border, unsigned char* out_u8, float* out_f32,
+                          long long* fallbacks);
 /* Convenience signature from the north star: parameters chosen on the host
  * like the CLI's `filter --eps` (eps_or_K < 1: tolerance) or `--K` (integer
  * eps_or_K >= 1: fixed K, T scanned over 1..10R); Gaussian range kernel,
- * R = 255, symmetric border. */
+ * R = 255, symmetric border. The period scans run on the GPU
+ * (fbf_select_params_gpu: same K, T, c as the host scan). */
 int fbf_filter(const float* img, int height, int width, double theta, double sigma,
                double eps_or_K, float* out);
 
@@ -149,6 +182,25 @@ int fbf_filter(const float* img, int height, int width, double theta, double sig
  * FBF_ERANGE. */
 int fbf_validate_f32_device(const float* d_img, size_t n, int R, int device, void* stream);
 
+/* ---- L3 reference filter and metrics on the GPU (fbf_brute.cu) ---------- */
+/* brute_bilateral (filter.cpp:83-127): the direct (2r+1)^2 bilateral filter
+ * with the range kernel read from its lattice (range[2R+1], phi(t) =
+ * range[t + R], t = lround(neighbour - centre)). FP64 with the reference's
+ * operation order and no FMA contraction: on float32 inputs the output equals
+ * the reference's compiled brute_bilateral bit for bit. out is double (the
+ * reference's GrayImage). Radius ceil(3 theta) <= 64. */
+int fbf_brute_bilateral_f32(const float* img, int width, int height, double theta, const double* range, int R,
+                            int border, double* out, long long* fallbacks);
+/* Same on device buffers (no intensity validation), enqueued on `stream`;
+ * returns after the kernel finished. */
+int fbf_brute_bilateral_f32_device(const float* d_img, int width, int height, double theta, const double* range,
+                                   int R, int border, double* d_out, unsigned long long* d_fallbacks, int device,
+                                   void* stream);
+/* compare_images (metrics.cpp:10-26) of a double reference image and a float
+ * candidate, both on the device: MSE, PSNR = 10 log10(255^2 / MSE) (+inf when
+ * equal) and max |difference|. Deterministic (fixed reduction order). */
+int fbf_compare_images_device(const double* d_ref, const float* d_cand, size_t n, double* mse, double* psnr_db,
+                              double* max_abs, int device, void* stream);
 /* ---- L4 synthetic inputs (synthetic.cpp + BASELINE.json generators) ------ */
 /* random_image (synthetic.cpp:25-31), scene_image (:33-64), as float32. */
 void fbf_random_image_f32(int width, int height, unsigned long long seed, float* out);

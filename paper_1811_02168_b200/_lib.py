@@ -43,6 +43,11 @@ SIGNATURES = {
     "fbf_min_error_over_period": (_i, [_dp, _i, _i, _i, _i, _ip, _dp]),
     "fbf_optimize_parameters": (_i, [_dp, _i, _d, _i, _i, _i, _ip, _ip, _dp, _i, _dp, _dp, _ip]),
     "fbf_select_params": (_i, [_i, _d, _i, _d, _i, _i, _i, _i, _ip, _ip, _dp, _i, _dp]),
+    "fbf_scan_period_errors_gpu": (_i, [_dp, _i, _i, _i, _i, _i, _dp]),
+    "fbf_scan_gpu_max_order": (_i, [_i]),
+    "fbf_min_error_over_period_gpu": (_i, [_dp, _i, _i, _i, _i, _ip, _dp]),
+    "fbf_optimize_parameters_gpu": (_i, [_dp, _i, _d, _i, _i, _i, _ip, _ip, _dp, _i, _dp, _dp, _ip]),
+    "fbf_select_params_gpu": (_i, [_i, _d, _i, _d, _i, _i, _i, _i, _ip, _ip, _dp, _i, _dp]),
     "fbf_fast_bilateral_f32": (_i, [_fp, _i, _i, _d, _i, _i, _i, _dp, _i, _fp, _llp]),
     "fbf_fast_bilateral_f32_device": (_i, [_vp, _i, _i, _d, _i, _i, _i, _dp, _i, _vp, _vp, _i, _vp]),
     "fbf_fast_bilateral_batch_f32": (_i, [_fp, _i, _i, _i, _d, _i, _i, _i, _dp, _i, _fp, _llp, _i]),
@@ -50,8 +55,12 @@ SIGNATURES = {
     "fbf_fast_bilateral_band_f32_device": (_i, [_vp, _i, _i, _i, _i, _i, _i, _d, _i, _i, _i, _dp, _i,
                                                 _vp, _vp, _i, _vp]),
     "fbf_band_source_rows": (_i, [_i, _i, _i, _d, _i, _ip, _ip]),
+    "fbf_fast_bilateral_u8": (_i, [_vp, _i, _i, _d, _i, _i, _i, _dp, _i, _vp, _vp, _llp]),
     "fbf_filter": (_i, [_fp, _i, _i, _d, _d, _d, _fp]),
     "fbf_validate_f32_device": (_i, [_vp, ctypes.c_size_t, _i, _i, _vp]),
+    "fbf_brute_bilateral_f32": (_i, [_fp, _i, _i, _d, _dp, _i, _i, _dp, _llp]),
+    "fbf_brute_bilateral_f32_device": (_i, [_vp, _i, _i, _d, _dp, _i, _i, _vp, _vp, _i, _vp]),
+    "fbf_compare_images_device": (_i, [_vp, _vp, ctypes.c_size_t, _dp, _dp, _dp, _i, _vp]),
     "fbf_random_image_f32": (None, [_i, _i, ctypes.c_ulonglong, _fp]),
     "fbf_scene_image_f32": (None, [_i, _i, ctypes.c_ulonglong, _fp]),
     "fbf_voronoi_image_f32": (None, [_i, _i, _i, _d, ctypes.c_ulonglong, _i, _fp]),

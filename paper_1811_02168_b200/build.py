@@ -26,6 +26,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
                      f"-I{os.path.join(ROOT, 'include')}"]
 CXX_FLAGS = ["-O3", "-std=c++20", "-fPIC", "-pthread", f"-I{os.path.join(ROOT, 'include')}"]
+# host library + auxiliary kernels (period scan, brute filter, 8-bit I/O)
+HOST_CU = ["fbf_api.cu", "fbf_scan.cu", "fbf_brute.cu"]
 # radius ranges per kernel translation unit (big radii are the slow ones)
 RADIUS_SPLITS = [(1, 8), (9, 12), (13, 15), (16, 18), (19, 21), (22, 24), (25, 26), (27, 28),
                  (29, 30), (31, 32)]
@@ -83,9 +85,10 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, o
         objs.append(obj)
         tasks.append(([nvcc, *NVCC_FLAGS, *extra, f"-DFBF_R_LO={lo}", f"-DFBF_R_HI={hi}", "-c",
                        os.path.join(CSRC, "fbf_kernel_inst.cu"), "-o", obj], obj + ".log"))
-    obj = os.path.join(build_dir, "fbf_api.o")
-    objs.append(obj)
-    tasks.append(([nvcc, *NVCC_FLAGS, *extra, "-c", os.path.join(CSRC, "fbf_api.cu"), "-o", obj], obj + ".log"))
+    for src in HOST_CU:
+        obj = os.path.join(build_dir, src.replace(".cu", ".o"))
+        objs.append(obj)
+        tasks.append(([nvcc, *NVCC_FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj], obj + ".log"))
     for src in ("fbf_params.cpp", "fbf_synth.cpp"):
         obj = os.path.join(build_dir, src.replace(".cpp", ".o"))
         objs.append(obj)

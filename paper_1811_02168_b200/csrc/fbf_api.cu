@@ -100,6 +100,18 @@ __global__ void validate_kernel(const float* __restrict__ img, size_t n, float R
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
 }
 
+// 8-bit I/O (imageio.cpp:53-101): bytes widen exactly to float; results are
+// written like the CLI's write_clamped + write_pgm (fourierbf.cpp:71-76,
+// imageio.cpp:83-89): clamp to [0, 255], round half away from zero
+__global__ void u8_to_f32_kernel(const unsigned char* __restrict__ in, float* __restrict__ out, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = (float)in[i];
+}
+__global__ void f32_to_u8_kernel(const float* __restrict__ in, unsigned char* __restrict__ out, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = (unsigned char)roundf(fminf(255.f, fmaxf(0.f, in[i])));
+}
+
 }  // namespace
 }  // namespace fbf_dev
 
@@ -457,8 +469,17 @@ int extent_of(bool bands, int height, int n_frames) { return bands ? height : n_
 // the kernel of piece i; intensity validation is fused into the kernel. Bands read the full device image, so their
 // halos need no extra copies: a band's kernel waits for the copy of the last
 // chunk its border-mapped window reaches. Results are identical to one launch.
-int filter_frames_on_device(int dev, const float* img, int n_frames, int width, int height, double theta,
-                            const Approx& a, int border, float* out, long long* fallbacks) {
+// Host buffers of a call: float32, or 8-bit (PGM payloads) widened / rounded on the device.
+struct HostIO {
+    const void* in;
+    void* out;
+    bool in_u8 = false, out_u8 = false;
+    size_t in_elem() const { return in_u8 ? 1 : sizeof(float); }
+    size_t out_elem() const { return out_u8 ? 1 : sizeof(float); }
+};
+
+int filter_frames_on_device(int dev, const HostIO& io, int n_frames, int width, int height, double theta,
+                            const Approx& a, int border, long long* fallbacks) {
     DeviceCtx* ctx = nullptr;
     int rc = get_ctx(dev, &ctx);
     if (rc != FBF_OK) return rc;
@@ -468,11 +489,16 @@ int filter_frames_on_device(int dev, const float* img, int n_frames, int width, 
     const size_t pixels = (size_t)n_frames * fp;
     const size_t img_bytes = align_up(pixels * sizeof(float));
     const size_t scr = align_up(scratch_bytes(a, theta, pixels));
-    rc = ctx->reserve(2 * img_bytes + scr);
+    const size_t u8_bytes = align_up(pixels);
+    const size_t in8 = io.in_u8 ? u8_bytes : 0, out8 = io.out_u8 ? u8_bytes : 0;
+    rc = ctx->reserve(2 * img_bytes + scr + in8 + out8);
     if (rc != FBF_OK) return rc;
     float* d_in = (float*)ctx->arena;
     float* d_out = (float*)((char*)ctx->arena + img_bytes);
     float2* d_scr = scr ? (float2*)((char*)ctx->arena + 2 * img_bytes) : nullptr;
+    unsigned char* d_in8 = (unsigned char*)ctx->arena + 2 * img_bytes + scr;
+    unsigned char* d_out8 = d_in8 + in8;
+    const int cvt_grid = ctx->num_sms * 8;
     cudaStream_t sc = ctx->stream, si = ctx->stream_in, so = ctx->stream_out;
     unsigned int* d_flag = (unsigned int*)(ctx->d_counters + 1);
     const int r = (int)std::ceil(3.0 * theta);
@@ -506,7 +532,16 @@ int filter_frames_on_device(int dev, const float* img, int n_frames, int width, 
     mark("start", si);
     for (int i = 0; i < pieces; ++i) {
         const size_t off = (size_t)lo[i] * unit, n = (size_t)(lo[i + 1] - lo[i]) * unit;
-        FBF_CUDA(cudaMemcpyAsync(d_in + off, img + off, n * sizeof(float), cudaMemcpyHostToDevice, si), "H2D");
+        if (io.in_u8) {
+            FBF_CUDA(cudaMemcpyAsync(d_in8 + off, (const unsigned char*)io.in + off, n, cudaMemcpyHostToDevice, si),
+                     "H2D");
+            fbf_dev::u8_to_f32_kernel<<<cvt_grid, 256, 0, si>>>(d_in8 + off, d_in + off, n);
+            FBF_CUDA(cudaGetLastError(), "u8 widen launch");
+            g_launches += 1;
+        } else {
+            FBF_CUDA(cudaMemcpyAsync(d_in + off, (const float*)io.in + off, n * sizeof(float), cudaMemcpyHostToDevice,
+                                     si), "H2D");
+        }
         mark("in", si);
         if ((rc = ctx->event(2 * i, &ev)) != FBF_OK) return rc;
         FBF_CUDA(cudaEventRecord(ev, si), "event");
@@ -530,11 +565,20 @@ int filter_frames_on_device(int dev, const float* img, int n_frames, int width, 
         rc = run_job(*ctx, job, theta, a, border, sp, ctx->d_counters, sc, d_flag);
         if (rc != FBF_OK) return rc;
         mark("k1", sc);
+        const size_t off = (size_t)lo[i] * unit, n = (size_t)(lo[i + 1] - lo[i]) * unit;
+        if (io.out_u8) {
+            fbf_dev::f32_to_u8_kernel<<<cvt_grid, 256, 0, sc>>>(d_out + off, d_out8 + off, n);
+            FBF_CUDA(cudaGetLastError(), "u8 round launch");
+            g_launches += 1;
+        }
         if ((rc = ctx->event(2 * i + 1, &ev)) != FBF_OK) return rc;
         FBF_CUDA(cudaEventRecord(ev, sc), "event");
         FBF_CUDA(cudaStreamWaitEvent(so, ev, 0), "wait");
-        const size_t off = (size_t)lo[i] * unit, n = (size_t)(lo[i + 1] - lo[i]) * unit;
-        FBF_CUDA(cudaMemcpyAsync(out + off, d_out + off, n * sizeof(float), cudaMemcpyDeviceToHost, so), "D2H");
+        if (io.out_u8)
+            FBF_CUDA(cudaMemcpyAsync((unsigned char*)io.out + off, d_out8 + off, n, cudaMemcpyDeviceToHost, so), "D2H");
+        else
+            FBF_CUDA(cudaMemcpyAsync((float*)io.out + off, d_out + off, n * sizeof(float), cudaMemcpyDeviceToHost, so),
+                     "D2H");
         mark("out", so);
     }
     FBF_CUDA(cudaMemcpyAsync(ctx->h_counters, ctx->d_counters, 2 * sizeof(unsigned long long),
@@ -610,6 +654,18 @@ void source_window(int height, int out_row0, int out_rows, int r, int border, in
 }
 
 }  // namespace
+
+int device_context(int device, void** stream, std::mutex** mtx) {
+    DeviceCtx* ctx = nullptr;
+    const int rc = get_ctx(device, &ctx);
+    if (rc != FBF_OK) return rc;
+    *stream = ctx->stream;
+    *mtx = &ctx->mtx;
+    return FBF_OK;
+}
+
+void count_launch(unsigned long long n) { g_launches += n; }
+
 }  // namespace fbf_b200
 
 using namespace fbf_b200;
@@ -670,7 +726,8 @@ int fbf_fast_bilateral_f32(const float* img, int width, int height, double theta
     Approx a;
     rc = make_approx(K, T, R, coeffs, a);
     if (rc != FBF_OK) return rc;
-    rc = filter_frames_on_device(g_default_device.load(), img, 1, width, height, theta, a, border, out, fallbacks);
+    rc = filter_frames_on_device(g_default_device.load(), HostIO{img, out}, 1, width, height, theta, a, border,
+                                 fallbacks);
     if (rc == FBF_OK) clear_error();
     return rc;
 }
@@ -743,8 +800,8 @@ int fbf_fast_bilateral_batch_f32(const float* img, int n_frames, int width, int 
     std::vector<long long> fb(G, 0);
     rc = per_device(G, [&](int g) {
         const int f0 = (int)((long long)n_frames * g / G), f1 = (int)((long long)n_frames * (g + 1) / G);
-        return filter_frames_on_device(g, img + f0 * fp, f1 - f0, width, height, theta, a, border,
-                                       out + f0 * fp, &fb[g]);
+        return filter_frames_on_device(g, HostIO{img + f0 * fp, out + f0 * fp}, f1 - f0, width, height, theta, a,
+                                       border, &fb[g]);
     });
     if (rc != FBF_OK) return rc;
     if (fallbacks)
@@ -808,6 +865,23 @@ int fbf_fast_bilateral_bands_f32(const float* img, int width, int height, double
     return FBF_OK;
 }
 
+int fbf_fast_bilateral_u8(const unsigned char* img, int width, int height, double theta, int K, int T, int R,
+                          const double* coeffs, int border, unsigned char* out_u8, float* out_f32,
+                          long long* fallbacks) {
+    int r = 0;
+    int rc = check_args(width, height, theta, K, T, R, coeffs, border, &r);
+    if (rc != FBF_OK) return rc;
+    if (!out_u8 && !out_f32) return fail(FBF_EINVAL, "fast_bilateral_u8: no output buffer");
+    if (out_u8 && out_f32) return fail(FBF_EINVAL, "fast_bilateral_u8: give one output buffer");
+    Approx a;
+    rc = make_approx(K, T, R, coeffs, a);
+    if (rc != FBF_OK) return rc;
+    HostIO io{img, out_u8 ? (void*)out_u8 : (void*)out_f32, true, out_u8 != nullptr};
+    rc = filter_frames_on_device(g_default_device.load(), io, 1, width, height, theta, a, border, fallbacks);
+    if (rc == FBF_OK) clear_error();
+    return rc;
+}
+
 int fbf_filter(const float* img, int height, int width, double theta, double sigma, double eps_or_K,
                float* out) {
     // run_filter (tools/fourierbf.cpp:236-270) with the CLI defaults: Gaussian
@@ -817,9 +891,9 @@ int fbf_filter(const float* img, int height, int width, double theta, double sig
     std::vector<double> c(2 * R + 1);
     int K = 0, T = 0;
     double err = 0.0;
-    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-    int rc = fbf_select_params(FBF_KERNEL_GAUSSIAN, sigma, R, is_K ? 0.0 : eps_or_K, is_K ? (int)eps_or_K : 0, 0,
-                               0, hw, &K, &T, c.data(), (int)c.size(), &err);
+    // period scans on the GPU (same K, T, c as the host scan: fbf_scan.cu)
+    int rc = fbf_select_params_gpu(FBF_KERNEL_GAUSSIAN, sigma, R, is_K ? 0.0 : eps_or_K, is_K ? (int)eps_or_K : 0,
+                                   0, 0, g_default_device.load(), &K, &T, c.data(), (int)c.size(), &err);
     if (rc != FBF_OK) return rc;
     return fbf_fast_bilateral_f32(img, width, height, theta, K, T, R, c.data(), FBF_BORDER_SYMMETRIC, out,
                                   nullptr);

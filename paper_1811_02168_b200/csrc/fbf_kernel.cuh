@@ -307,9 +307,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 // instructions). bar.arrive / bar.sync order shared-memory accesses among the
 // participating threads.
 __device__ __forceinline__ void named_arrive(int id, int nthreads) {
+#ifdef FBF_DEV_PAIRONLY  // dev: FFMA2 warps alone, no handoffs (results invalid)
+    return;
+#endif
     asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
+#ifdef FBF_DEV_PAIRONLY
+    return;
+#endif
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 // barrier ids (0 is __syncthreads): gen full/empty, column full/empty, f stage empty
@@ -972,6 +978,9 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
         gstep += steps;
     }
     };  // run_roles
+#ifdef FBF_DEV_PAIRONLY
+    if (role != kRoleRow) role = kRoleIdle;
+#endif
     if (role != kRoleIdle) run_roles(std::true_type{});
     if (role == kRoleComb && p.fallbacks) {
         const unsigned w = __reduce_add_sync(0xffffffffu, n_fallbacks);

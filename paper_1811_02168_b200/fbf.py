@@ -250,13 +250,34 @@ class PeriodScanResult:
     best_error: float
 
 
+def scan_period_errors_gpu(samples: RangeKernelSamples, k_lo: int, n_orders: int, t_max: int,
+                           device: int = 0) -> np.ndarray:
+    """E(K, T) for K in [k_lo, k_lo + n_orders), T in 1..t_max on the GPU
+    (fbf_scan.cu); shape (n_orders, t_max). ~1e-15 relative to scan_period_errors
+    near the minimum."""
+    e = np.zeros((max(1, n_orders), max(1, t_max)))
+    _check(_lib.load().fbf_scan_period_errors_gpu(_dptr(samples.values), samples.dynamic_range, k_lo, n_orders,
+                                                  t_max, device, _dptr(e)))
+    return e
+
+
+def scan_gpu_max_order(dynamic_range: int = 255) -> int:
+    return int(_lib.load().fbf_scan_gpu_max_order(dynamic_range))
+
+
 def min_error_over_period(terms: int, samples: RangeKernelSamples, t_max: int,
-                          threads: int = 1) -> PeriodScanResult:
-    """approx.cpp:132-144."""
+                          threads: int = 1, device: int | None = None) -> PeriodScanResult:
+    """approx.cpp:132-144 (device: GPU scan + exact host re-check, same result)."""
     T = ctypes.c_int(0)
     e = ctypes.c_double(0)
-    _check(_lib.load().fbf_min_error_over_period(_dptr(samples.values), samples.dynamic_range, terms, t_max,
-                                                 threads, ctypes.byref(T), ctypes.byref(e)))
+    lib = _lib.load()
+    if device is None:
+        rc = lib.fbf_min_error_over_period(_dptr(samples.values), samples.dynamic_range, terms, t_max,
+                                           threads, ctypes.byref(T), ctypes.byref(e))
+    else:
+        rc = lib.fbf_min_error_over_period_gpu(_dptr(samples.values), samples.dynamic_range, terms, t_max,
+                                               int(device), ctypes.byref(T), ctypes.byref(e))
+    _check(rc)
     return PeriodScanResult(T.value, e.value)
 
 
@@ -273,6 +294,7 @@ class OptimizeOptions:
     t_max: int = 0
     k_max: int = 0
     threads: int = 1
+    device: int | None = None  # B200 extension: period scans on this CUDA device (fbf_scan.cu)
 
 
 @dataclass
@@ -302,8 +324,14 @@ def optimize_parameters(samples: RangeKernelSamples, tolerance: float,
     per = np.zeros(3 * cap)
     K, T, n = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
     e = ctypes.c_double(0)
-    rc = _lib.load().fbf_optimize_parameters(_dptr(samples.values), R, float(tolerance), o.t_max, o.k_max,
-                                             o.threads, ctypes.byref(K), ctypes.byref(T), _dptr(c), cap,
+    lib = _lib.load()
+    if o.device is None:
+        rc = lib.fbf_optimize_parameters(_dptr(samples.values), R, float(tolerance), o.t_max, o.k_max,
+                                         o.threads, ctypes.byref(K), ctypes.byref(T), _dptr(c), cap,
+                                         ctypes.byref(e), _dptr(per), ctypes.byref(n))
+    else:
+        rc = lib.fbf_optimize_parameters_gpu(_dptr(samples.values), R, float(tolerance), o.t_max, o.k_max,
+                                             int(o.device), ctypes.byref(K), ctypes.byref(T), _dptr(c), cap,
                                              ctypes.byref(e), _dptr(per), ctypes.byref(n))
     if rc not in (FBF_OK, FBF_EUNREACHABLE):
         _check(rc)
@@ -316,15 +344,22 @@ def optimize_parameters(samples: RangeKernelSamples, tolerance: float,
 
 def select_parameters(sigma: float, *, eps: float | None = None, K: int | None = None, T: int | None = None,
                       method: str = "fast", kernel: str = "gaussian", dynamic_range: int = 255,
-                      threads: int = 1) -> FourierApproximation:
-    """CLI select_parameters (tools/fourierbf.cpp:185-234)."""
+                      threads: int = 1, device: int | None = None) -> FourierApproximation:
+    """CLI select_parameters (tools/fourierbf.cpp:185-234). device: run the
+    period scans on that CUDA device (same K, T and coefficients as the host
+    scan: near-minimal T are re-fitted on the host)."""
     R = dynamic_range
     c = np.zeros(2 * R + 1)
     Ko, To = ctypes.c_int(0), ctypes.c_int(0)
     e = ctypes.c_double(0)
-    rc = _lib.load().fbf_select_params(int(RangeKernelKind[kernel]), float(sigma), R, float(eps or 0.0),
-                                       int(K or 0), int(T or 0), int(method == "fbf"), threads,
-                                       ctypes.byref(Ko), ctypes.byref(To), _dptr(c), c.size, ctypes.byref(e))
+    lib = _lib.load()
+    head = (int(RangeKernelKind[kernel]), float(sigma), R, float(eps or 0.0), int(K or 0), int(T or 0),
+            int(method == "fbf"))
+    tail = (ctypes.byref(Ko), ctypes.byref(To), _dptr(c), c.size, ctypes.byref(e))
+    if device is None:
+        rc = lib.fbf_select_params(*head, threads, *tail)
+    else:
+        rc = lib.fbf_select_params_gpu(*head, int(device), *tail)
     if rc == FBF_EUNREACHABLE:
         rep = OptimizationReport(Ko.value, To.value, c[:Ko.value].copy(), e.value, float(eps or 0), 10 * R, [])
         raise ToleranceUnreachable(_lib.last_error(), rep)
@@ -369,6 +404,30 @@ def fast_bilateral(img, kernel: SpatialKernel, approx: FourierApproximation,
     _check(_lib.load().fbf_fast_bilateral_f32(_fptr(a), a.shape[1], a.shape[0], kernel.theta, approx.terms,
                                               approx.half_period, approx.dynamic_range, _dptr(c), _border(border),
                                               _fptr(out), ctypes.byref(fb)))
+    if diag is not None:
+        diag.fallback_pixels += fb.value
+    return out
+
+
+def fast_bilateral_u8(img, kernel: SpatialKernel, approx: FourierApproximation,
+                      border=BorderPolicy.symmetric, diag: FilterDiagnostics | None = None,
+                      out_dtype=np.uint8) -> np.ndarray:
+    """fast_bilateral on an 8-bit image (a PGM payload): 1 byte per pixel crosses
+    PCIe. out_dtype uint8: clamped to [0,255] and rounded half away from zero
+    on the device (the CLI's write_clamped + write_pgm); float32: the float result."""
+    a = np.ascontiguousarray(img, dtype=np.uint8)
+    if a.ndim != 2:
+        raise InvalidArgument("GrayImage: expected a 2-D (height, width) array")
+    c = _approx_args(approx)
+    out = np.empty(a.shape, dtype=np.dtype(out_dtype))
+    if out.dtype not in (np.uint8, np.float32):
+        raise InvalidArgument("fast_bilateral_u8: out_dtype must be uint8 or float32")
+    fb = ctypes.c_longlong(0)
+    o8 = ctypes.c_void_p(out.ctypes.data) if out.dtype == np.uint8 else None
+    o32 = ctypes.c_void_p(out.ctypes.data) if out.dtype == np.float32 else None
+    _check(_lib.load().fbf_fast_bilateral_u8(ctypes.c_void_p(a.ctypes.data), a.shape[1], a.shape[0],
+                                             kernel.theta, approx.terms, approx.half_period, approx.dynamic_range,
+                                             _dptr(c), _border(border), o8, o32, ctypes.byref(fb)))
     if diag is not None:
         diag.fallback_pixels += fb.value
     return out
@@ -469,6 +528,124 @@ def fbf_filter(img, theta: float, sigma: float, eps_or_K: float) -> np.ndarray:
     _check(_lib.load().fbf_filter(_fptr(a), a.shape[0], a.shape[1], float(theta), float(sigma), float(eps_or_K),
                                   _fptr(out)))
     return out
+
+
+# ---- brute filter and metrics (filter.cpp:83-127, metrics.hpp) --------------
+
+def brute_bilateral(img, kernel: SpatialKernel, range_samples: RangeKernelSamples,
+                    border=BorderPolicy.symmetric, diag: FilterDiagnostics | None = None) -> np.ndarray:
+    """filter.hpp:35-38 / filter.cpp:83-127 on the GPU: FP64 output equal to the
+    reference's brute_bilateral bit for bit on float32 inputs (fbf_brute.cu)."""
+    a = _as_image(img)
+    out = np.empty(a.shape, dtype=np.float64)
+    fb = ctypes.c_longlong(0)
+    _check(_lib.load().fbf_brute_bilateral_f32(_fptr(a), a.shape[1], a.shape[0], float(kernel.theta),
+                                               _dptr(np.ascontiguousarray(range_samples.values, dtype=np.float64)),
+                                               range_samples.dynamic_range, _border(border), _dptr(out),
+                                               ctypes.byref(fb)))
+    if diag is not None:
+        diag.fallback_pixels += fb.value
+    return out
+
+
+def brute_bilateral_device(d_img, kernel: SpatialKernel, range_samples: RangeKernelSamples, d_out,
+                           border=BorderPolicy.symmetric, d_fallbacks=None, stream=None) -> None:
+    """Device-resident brute filter: d_img float32 (H, W), d_out float64 (H, W) CUDA tensors."""
+    import torch
+    if d_img.dtype != torch.float32 or d_out.dtype != torch.float64 or not d_img.is_contiguous():
+        raise InvalidArgument("brute_bilateral_device: float32 input and float64 output tensors")
+    H, W = d_img.shape
+    st = stream if stream is not None else torch.cuda.current_stream(d_img.device)
+    _check(_lib.load().fbf_brute_bilateral_f32_device(
+        ctypes.c_void_p(d_img.data_ptr()), W, H, float(kernel.theta),
+        _dptr(np.ascontiguousarray(range_samples.values, dtype=np.float64)), range_samples.dynamic_range,
+        _border(border), ctypes.c_void_p(d_out.data_ptr()),
+        ctypes.c_void_p(d_fallbacks.data_ptr() if d_fallbacks is not None else 0), d_img.device.index,
+        ctypes.c_void_p(st.cuda_stream)))
+
+
+@dataclass
+class ImageDelta:
+    """metrics.hpp:11-15."""
+    mse: float = 0.0
+    psnr_db: float = 0.0
+    max_abs_err: float = 0.0
+
+
+def compare_images(a, b) -> ImageDelta:
+    """metrics.cpp:10-26 on host arrays."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if a.shape != b.shape:
+        raise InvalidArgument("compare_images: dimension mismatch")
+    d = a - b
+    mse = float(np.sum(d * d) / d.size)
+    psnr = 10.0 * math.log10(255.0 * 255.0 / mse) if mse > 0 else math.inf
+    return ImageDelta(mse, psnr, float(np.max(np.abs(d))) if d.size else 0.0)
+
+
+def compare_images_device(d_ref, d_cand, stream=None) -> ImageDelta:
+    """compare_images of a float64 reference and a float32 candidate CUDA tensor
+    (full-size accuracy check without a host round trip)."""
+    import torch
+    if d_ref.shape != d_cand.shape:
+        raise InvalidArgument("compare_images: dimension mismatch")
+    st = stream if stream is not None else torch.cuda.current_stream(d_ref.device)
+    mse, psnr, mx = ctypes.c_double(0), ctypes.c_double(0), ctypes.c_double(0)
+    _check(_lib.load().fbf_compare_images_device(ctypes.c_void_p(d_ref.data_ptr()), ctypes.c_void_p(d_cand.data_ptr()),
+                                                 d_ref.numel(), ctypes.byref(mse), ctypes.byref(psnr),
+                                                 ctypes.byref(mx), d_ref.device.index,
+                                                 ctypes.c_void_p(st.cuda_stream)))
+    return ImageDelta(mse.value, psnr.value, mx.value)
+
+
+def prop1_bound(eps: float, dynamic_range: int, omega0: float = 1.0) -> float:
+    """metrics.cpp:28-32: 2 R eps / (omega0 - eps)."""
+    if not (eps > 0.0) or not (eps < omega0):
+        raise InvalidArgument("prop1_bound: requires 0 < eps < omega(0)")
+    return 2.0 * dynamic_range * eps / (omega0 - eps)
+
+
+def kernel_error(samples: RangeKernelSamples, approx: FourierApproximation) -> float:
+    """metrics.cpp:34-44: sum_t (phi(t) - phihat(t))^2."""
+    if samples.dynamic_range != approx.dynamic_range:
+        raise InvalidArgument("kernel_error: dynamic range mismatch")
+    R = samples.dynamic_range
+    s = 0.0
+    for t in range(-R, R + 1):
+        d = samples.at(t) - approx.evaluate(t)
+        s += d * d
+    return s
+
+
+@dataclass
+class ComparisonResult:
+    """metrics.hpp:30-43."""
+    mse: float = 0.0
+    psnr_db: float = 0.0
+    max_abs_err: float = 0.0
+    prop1_bound: float = 0.0
+    bound_satisfied: bool = False
+
+    @staticmethod
+    def csv_header() -> str:
+        return "mse,psnr_db,max_abs_err,prop1_bound,bound_satisfied"
+
+    def to_csv(self) -> str:
+        psnr = "inf" if math.isinf(self.psnr_db) else f"{self.psnr_db:.17g}"
+        return (f"{self.mse:.17g},{psnr},{self.max_abs_err:.17g},{self.prop1_bound:.17g},"
+                f"{'true' if self.bound_satisfied else 'false'}")
+
+
+def compare_with_bound(reference, candidate, achieved_kernel_error: float, dynamic_range: int,
+                       omega0: float = 1.0) -> ComparisonResult:
+    """metrics.cpp:58-70 (host arrays, or a float64/float32 CUDA tensor pair)."""
+    if hasattr(reference, "is_cuda") and reference.is_cuda:
+        d = compare_images_device(reference, candidate)
+    else:
+        d = compare_images(reference, candidate)
+    b = prop1_bound(achieved_kernel_error, dynamic_range, omega0)
+    return ComparisonResult(d.mse, d.psnr_db, d.max_abs_err, b, d.max_abs_err <= b)
 
 
 # ---- synthetic inputs (synthetic.cpp + BASELINE.json generators) ----------

@@ -1,0 +1,237 @@
+"""GPU tests of the components next to the hot path:
+
+  * the period scan on the GPU (fbf_scan.cu) -- errors within 1e-9 relative of
+    the host scan, and selections (K, T, c, E) identical to the host's,
+    including the reference's frozen optimiser values (test_approx.cpp);
+  * the direct filter on the GPU (fbf_brute.cu) -- bit-identical to the
+    reference's brute_bilateral (golden fixture + oracle/_ref live), all borders;
+  * device-side compare_images / Prop. 1 bound at a full config size;
+  * the 8-bit host path (fbf_fast_bilateral_u8) against the float path;
+  * the CLI (filter / compare / optimize) end to end.
+"""
+import math
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def samples(fb, kind, sigma, R=255):
+    return fb.sample_range_kernel(fb.RangeKernelSpec(fb.RangeKernelKind[kind], sigma, R))
+
+
+# ---- period scan -------------------------------------------------------------
+
+@pytest.mark.parametrize("kind,sigma", [("gaussian", 50.0), ("gaussian", 15.0), ("exponential", 20.0),
+                                        ("cauchy", 40.0)])
+def test_gpu_scan_errors_match_host(gpu, kind, sigma):
+    fb = gpu
+    b = samples(fb, kind, sigma)
+    eg = fb.scan_period_errors_gpu(b, 1, 10, 2550, 0)
+    for K in (1, 2, 4, 7, 10):
+        eh = fb.scan_period_errors(K, b, 2550, threads=8)
+        rel = np.abs(eg[K - 1] - eh) / np.maximum(np.abs(eh), 1e-300)
+        # ill-conditioned design matrices (large T, errors far above the minimum)
+        # round differently in the tree reductions; near the minimum they agree
+        assert rel.max() < 1e-5, (K, rel.max(), int(rel.argmax()) + 1)
+        near = eh <= 2.0 * eh.min()
+        assert rel[near].max() < 1e-10, (K, rel[near].max())
+        assert int(np.argmin(eg[K - 1])) == int(np.argmin(eh))
+
+
+def test_gpu_scan_reproduces_reference_pins(gpu):
+    # test_approx.cpp:86,105,129-130,223-225 (frozen values of the reference build)
+    fb = gpu
+    b50 = samples(fb, "gaussian", 50.0)
+    e = fb.scan_period_errors_gpu(b50, 4, 1, 400, 0)[0]
+    assert abs(e[202] - 0.0096065911564679699) <= 1e-8 * 0.0096065911564679699
+    r = fb.min_error_over_period(4, b50, 400, device=0)
+    assert r.best_half_period == 203
+    assert r.best_error == fb.min_error_over_period(4, b50, 400).best_error
+    rep = fb.optimize_parameters(b50, 0.01, fb.OptimizeOptions(t_max=400, device=0))
+    assert (rep.best_terms, rep.best_half_period) == (4, 203)
+    b40 = samples(fb, "gaussian", 40.0)
+    r = fb.min_error_over_period(4, b40, 2550, device=0)
+    assert r.best_half_period == 179
+    assert abs(r.best_error - 0.039303651041756635) <= 1e-6 * 0.039303651041756635
+
+
+@pytest.mark.parametrize("sigma,eps", [(30.0, 0.1), (15.0, 0.01), (80.0, 0.05), (10.0, 0.05), (120.0, 0.001),
+                                       (5.0, 0.1)])
+def test_gpu_selection_identical_to_host(gpu, sigma, eps):
+    fb = gpu
+    b = samples(fb, "gaussian", sigma)
+    h = fb.optimize_parameters(b, eps, fb.OptimizeOptions(threads=8))
+    g = fb.optimize_parameters(b, eps, fb.OptimizeOptions(device=0))
+    assert (g.best_terms, g.best_half_period) == (h.best_terms, h.best_half_period)
+    assert np.array_equal(g.coefficients, h.coefficients)
+    assert g.achieved_error == h.achieved_error
+    assert [(p.terms, p.best_half_period, p.best_error) for p in g.per_order] == \
+           [(p.terms, p.best_half_period, p.best_error) for p in h.per_order]
+
+
+def test_gpu_select_params_cli_modes(gpu):
+    fb = gpu
+    for kw in (dict(eps=0.1), dict(K=4), dict(K=3, T=100), dict(eps=0.05, method="fbf"), dict(K=5, method="fbf")):
+        h = fb.select_parameters(50.0, **kw)
+        g = fb.select_parameters(50.0, device=0, **kw)
+        assert (g.terms, g.half_period) == (h.terms, h.half_period), kw
+        assert np.array_equal(g.coefficients, h.coefficients), kw
+
+
+def test_gpu_scan_unreachable_and_capacity(gpu):
+    fb = gpu
+    b = samples(fb, "gaussian", 30.0, R=7)   # test_approx.cpp:153-181 style: small R saturates
+    with pytest.raises(fb.ToleranceUnreachable) as gi:
+        fb.optimize_parameters(b, 1e-40, fb.OptimizeOptions(t_max=3, device=0))
+    with pytest.raises(fb.ToleranceUnreachable) as hi:
+        fb.optimize_parameters(b, 1e-40, fb.OptimizeOptions(t_max=3))
+    assert gi.value.best_found.best_terms == hi.value.best_found.best_terms
+    assert gi.value.best_found.best_half_period == hi.value.best_found.best_half_period
+    kmax = fb.scan_gpu_max_order(255)
+    with pytest.raises(fb.InvalidArgument):
+        fb.scan_period_errors_gpu(samples(fb, "gaussian", 30.0), kmax, 2, 10, 0)
+
+
+# ---- brute filter --------------------------------------------------------------
+
+def test_gpu_brute_bit_exact_golden(gpu, oracle, golden):
+    fb = gpu
+    img = golden["scene_96x96_2024"].astype(np.float32)
+    rng = fb.RangeKernelSamples(255, oracle.range_samples("gaussian", 55.0))
+    diag = fb.FilterDiagnostics()
+    out = fb.brute_bilateral(img, fb.build_spatial_kernel(5.0), rng, "symmetric", diag)
+    assert np.array_equal(out, golden["brute_scene96_t5_s55"])
+    assert diag.fallback_pixels == 0
+
+
+@pytest.mark.parametrize("border", ["symmetric", "replicate", "zero"])
+def test_gpu_brute_bit_exact_reference_live(gpu, ref_lib, border):
+    fb = gpu
+    rs = np.random.default_rng(7)
+    for (w, h, theta, sigma, integer) in [(37, 29, 2.0, 30.0, True), (64, 48, 3.3, 12.0, False),
+                                          (5, 4, 3.0, 50.0, False), (70, 33, 6.0, 80.0, True)]:
+        img = rs.uniform(0, 255, (h, w)).astype(np.float32)
+        if integer:
+            img = np.round(img)
+        rng = ref_lib.range_samples("gaussian", sigma)
+        ref, ref_fb = ref_lib.brute_bilateral(img.astype(np.float64), theta, rng, border=border)
+        diag = fb.FilterDiagnostics()
+        out = fb.brute_bilateral(img, fb.build_spatial_kernel(theta), fb.RangeKernelSamples(255, rng), border, diag)
+        assert np.array_equal(out, ref), (w, h, theta, border, np.abs(out - ref).max())
+        assert diag.fallback_pixels == ref_fb
+
+
+def test_gpu_brute_fallback_and_errors(gpu):
+    fb = gpu
+    img = np.full((6, 7), 200.0, np.float32)
+    zero = fb.RangeKernelSamples(255, np.zeros(511))   # den = 0 everywhere -> every pixel falls back
+    diag = fb.FilterDiagnostics()
+    out = fb.brute_bilateral(img, fb.build_spatial_kernel(1.0), zero, "symmetric", diag)
+    assert diag.fallback_pixels == img.size and np.array_equal(out, img.astype(np.float64))
+    bad = img.copy()
+    bad[2, 3] = 300.0
+    with pytest.raises(fb.InvalidArgument):
+        fb.brute_bilateral(bad, fb.build_spatial_kernel(1.0), zero)
+    with pytest.raises(fb.InvalidArgument):
+        fb.brute_bilateral(img, fb.SpatialKernel(-1.0, 0, np.ones(1)), zero)
+
+
+def test_device_compare_and_prop1_bound_full_size(gpu):
+    # the full-size accuracy check of SURVEY §8f row 2: brute vs fast on the
+    # device at 2048x2048 (BASELINE config 1's image), Prop. 1 bound (metrics.cpp:58-70)
+    import torch
+    fb = gpu
+    from paper_1811_02168_b200 import configs
+    cfg = configs.CONFIGS["c1"]
+    img = configs.make_frame(cfg, 0)
+    b = samples(fb, "gaussian", cfg.sigma)
+    approx = configs.select(cfg)
+    k = fb.build_spatial_kernel(cfg.theta)
+    d_img = torch.from_numpy(img).cuda()
+    d_fast = torch.empty_like(d_img)
+    d_brute = torch.empty(img.shape, dtype=torch.float64, device="cuda")
+    fb.fast_bilateral_device(d_img, k, approx, d_fast)
+    fb.brute_bilateral_device(d_img, k, b, d_brute)
+    torch.cuda.synchronize()
+    achieved = fb.kernel_error(b, approx)
+    cmp = fb.compare_with_bound(d_brute, d_fast, achieved, 255)
+    host = fb.compare_images(d_brute.cpu().numpy(), d_fast.cpu().numpy())
+    assert math.isclose(cmp.mse, host.mse, rel_tol=1e-9)
+    assert cmp.max_abs_err == host.max_abs_err
+    assert cmp.bound_satisfied, cmp
+    assert cmp.psnr_db > 30.0, cmp
+
+
+# ---- 8-bit path -----------------------------------------------------------------
+
+def round_half_away(v):
+    v = np.clip(v.astype(np.float64), 0.0, 255.0)
+    return np.floor(v + 0.5)
+
+
+@pytest.mark.parametrize("border", ["symmetric", "zero"])
+def test_u8_path_matches_float_path(gpu, border):
+    fb = gpu
+    rs = np.random.default_rng(3)
+    img8 = rs.integers(0, 256, (300, 257), dtype=np.uint8)
+    k = fb.build_spatial_kernel(4.0)
+    a = fb.select_parameters(30.0, eps=0.1)
+    f32 = fb.fast_bilateral(img8.astype(np.float32), k, a, border)
+    o32 = fb.fast_bilateral_u8(img8, k, a, border, out_dtype=np.float32)
+    assert np.array_equal(o32, f32)   # same kernel on exactly widened bytes
+    o8 = fb.fast_bilateral_u8(img8, k, a, border)
+    assert o8.dtype == np.uint8
+    assert np.array_equal(o8, round_half_away(f32).astype(np.uint8))
+
+
+def test_u8_path_against_reference_rounding(gpu, oracle):
+    # the CLI's write_clamped + write_pgm of the reference's double result: equal
+    # except where the fp32/fp64 difference (~1e-4) straddles a .5 boundary
+    fb = gpu
+    img8 = np.asarray(oracle.random_image(120, 90, 11), dtype=np.uint8)
+    a = fb.select_parameters(40.0, eps=0.05)
+    ref, _ = oracle.fast_bilateral(img8.astype(np.float64), 3.0, a.terms, a.half_period, a.coefficients)
+    want = round_half_away(ref)
+    got = fb.fast_bilateral_u8(img8, fb.build_spatial_kernel(3.0), a).astype(np.float64)
+    assert np.abs(got - want).max() <= 1.0
+    assert np.mean(got == want) > 0.999
+
+
+# ---- CLI --------------------------------------------------------------------------
+
+def _cli(*args, cwd=None):
+    return subprocess.run([sys.executable, "-m", "paper_1811_02168_b200.cli", *args], cwd=ROOT,
+                          capture_output=True, text=True, timeout=600)
+
+
+def test_cli_filter_compare_optimize(gpu, tmp_path):
+    fb = gpu
+    from paper_1811_02168_b200.imageio import read_pgm, write_pgm
+    rs = np.random.default_rng(5)
+    img8 = rs.integers(0, 256, (64, 80), dtype=np.uint8)
+    src, dst, bru = tmp_path / "in.pgm", tmp_path / "out.pgm", tmp_path / "brute.pgm"
+    write_pgm(img8, str(src))
+    p = _cli("filter", "--in", str(src), "--out", str(dst), "--theta", "3", "--sigma", "30", "--eps", "0.1")
+    assert p.returncode == 0, p.stderr
+    a = fb.select_parameters(30.0, eps=0.1)
+    want = fb.fast_bilateral_u8(img8, fb.build_spatial_kernel(3.0), a)
+    assert np.array_equal(read_pgm(str(dst)), want)
+    assert "params: K=5 T=168" in p.stderr
+    p = _cli("--border", "zero", "filter", "--in", str(src), "--out", str(bru), "--theta", "2", "--sigma", "30",
+             "--method", "brute")
+    assert p.returncode == 0, p.stderr
+    p = _cli("compare", "--in", "synth:96x72", "--theta", "3", "--sigma", "30", "--eps", "0.05")
+    assert p.returncode == 0, p.stderr
+    head, row = p.stdout.strip().split("\n")
+    assert head == "mse,psnr_db,max_abs_err,prop1_bound,bound_satisfied"
+    assert row.endswith("true")
+    p = _cli("optimize", "--sigma", "50", "--eps", "0.01", "--tmax", "400")
+    assert p.returncode == 0, p.stderr
+    assert "K* = 4\nT* = 203" in p.stdout
