@@ -15,6 +15,7 @@
 #include <limits>
 #include <numbers>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/fbf.h"
@@ -278,20 +279,25 @@ int min_period(const double* samples, int R, int K, int t_max, ScanBackend& be, 
     double gmin = eg[0];
     for (int T = 2; T <= t_max; ++T) gmin = std::min(gmin, eg[T - 1]);
     const double limit = gmin + kRecheckWindow * std::fabs(gmin) + 1e-300;
-    bool any = false;
-    for (int T = 1; T <= t_max; ++T) {
-        if (!(eg[T - 1] <= limit)) continue;
+    std::vector<int> cand;
+    for (int T = 1; T <= t_max; ++T)
+        if (eg[T - 1] <= limit) cand.push_back(T);
+    if (cand.empty()) return fail(FBF_ECUDA, "gpu period scan: no finite error");
+    // exact host errors of the candidates (many for flat scans, e.g. K = 1 where
+    // E does not depend on T), on host threads; argmin in ascending T
+    std::vector<double> ex(cand.size(), 0.0);
+    std::vector<int> st(cand.size(), FBF_OK);
+    parallel_for(0, static_cast<int>(cand.size()), cand.size() > 16 ? be.threads : 1, [&](int i) {
         std::vector<double> c;
-        double e = 0.0;
-        const int rc = fit_fixed(samples, R, K, T, c, e);
-        if (rc != FBF_OK) return rc;
-        if (!any || e < e_best) {
-            T_best = T;
-            e_best = e;
-            any = true;
+        st[i] = fit_fixed(samples, R, K, cand[i], c, ex[i]);
+    });
+    for (size_t i = 0; i < cand.size(); ++i) {
+        if (st[i] != FBF_OK) return fail(st[i], "fit_coefficients: non-finite entries");
+        if (i == 0 || ex[i] < e_best) {
+            T_best = cand[i];
+            e_best = ex[i];
         }
     }
-    if (!any) return fail(FBF_ECUDA, "gpu period scan: no finite error");
     return FBF_OK;
 }
 
@@ -516,7 +522,7 @@ int fbf_optimize_parameters_gpu(const double* samples, int R, double tol, int t_
                                 double* per_order, int* n_orders) {
     ScanBackend be;
     be.device = device;
-    be.threads = 1;
+    be.threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
     return optimize_impl(samples, R, tol, t_max, k_max, be, K_out, T_out, coeffs, coeff_cap, err_out, per_order,
                          n_orders);
 }
@@ -533,7 +539,7 @@ int fbf_select_params_gpu(int kind, double sigma, int R, double eps, int K, int 
                           int* K_out, int* T_out, double* coeffs, int coeff_cap, double* err_out) {
     ScanBackend be;
     be.device = device;
-    be.threads = 1;
+    be.threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
     return select_impl(kind, sigma, R, eps, K, T, method_fbf, be, K_out, T_out, coeffs, coeff_cap, err_out);
 }
 
@@ -548,6 +554,7 @@ int fbf_min_error_over_period_gpu(const double* samples, int R, int K, int t_max
                                   double* err_out) {
     ScanBackend be;
     be.device = device;
+    be.threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
     int T = 1;
     double e = 0.0;
     const int rc = min_period(samples, R, K, t_max, be, T, e);
