@@ -119,6 +119,18 @@ int fbf_optimize_parameters_gpu(const double* samples, int R, double tol, int t_
                                 double* per_order, int* n_orders);
 int fbf_select_params_gpu(int kind, double sigma, int R, double eps, int K, int T, int method_fbf, int device,
                           int* K_out, int* T_out, double* coeffs, int coeff_cap, double* err_out);
+/* ---- L2 lookup table: lut.cpp -------------------------------------------- */
+/* build_lut (lut.cpp:61-113): K*[i*n_eps+j], T*[i*n_eps+j] of Algorithm 1 for
+ * the Gaussian kernel at (sigmas[i], epsilons[j]); grids strictly ascending
+ * (sigma, log10(1/eps)), >= 2 points each, eps in (0,1). device >= 0: period
+ * scans on that GPU (identical cells); device < 0: `threads` host threads.
+ * A cell that cannot reach its tolerance fails the build, cell identified. */
+int fbf_build_lut(const double* sigmas, int n_sigma, const double* epsilons, int n_eps, int R, int t_max,
+                  int device, int threads, int* K_out, int* T_out);
+/* query_lut (lut.cpp:116-143): bilinear in (sigma, log10(1/eps)), K rounded
+ * up, T to nearest; outside the grid FBF_ERANGE (std::out_of_range). */
+int fbf_query_lut(const double* sigma_grid, int n_sigma, const double* logeps_grid, int n_eps, const int* K,
+                  const int* T, double sigma, double eps, int* K_out, int* T_out);
 /* ---- L3 filter: filter.cpp (the hot path, sm_100a) ---------------------- */
 /* fast_bilateral (filter.hpp:43-46, filter.cpp:129-213) on HOST buffers:
  * validates intensities, copies img to the device, runs the fused kernel,

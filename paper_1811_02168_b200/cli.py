@@ -7,6 +7,8 @@ Commands and options follow fourierbf.cpp:278-374:
     filter   --in PGM|synth:WxH --out PGM --theta TH [--sigma S] [--eps E | --K K [--T T]]
              [--method fast|brute|fbf] [--kernel KIND] [--range R]
     compare  --in PGM|synth:WxH --theta TH --sigma S --eps E [--report CSV] [--kernel KIND] [--range R]
+    build-lut --sigmas S1,S2,... --epsilons E1,E2,... --out PATH [--range R] [--tmax N]
+    query-lut --lut PATH --sigma S --eps E
 KIND = gaussian | exponential | cauchy | table:<path>.
 
 What runs where: the fast filter is the fused sm_100a kernel; --method brute is
@@ -14,8 +16,8 @@ the direct filter on the GPU in FP64 (fbf_brute.cu, bit-identical to the
 reference's brute_bilateral); the period scans of the parameter search run on
 the GPU with an exact host re-check (fbf_scan.cu: the same K, T and
 coefficients as the reference's host scan; --device -1 keeps them on the host).
-8-bit PGM payloads cross PCIe as bytes (fbf_fast_bilateral_u8). The LUT
-commands (build-lut / query-lut) are not part of this GPU path.
+8-bit PGM payloads cross PCIe as bytes (fbf_fast_bilateral_u8). build-lut
+runs Algorithm 1 per grid cell with the GPU scans (lut.py).
 """
 from __future__ import annotations
 
@@ -26,6 +28,7 @@ import time
 import numpy as np
 
 from . import fbf
+from . import lut as L
 from .imageio import read_kernel_table, read_pgm, write_pgm
 
 
@@ -79,6 +82,12 @@ def select_parameters(args, samples: fbf.RangeKernelSamples, g) -> fbf.FourierAp
         raise ValueError("--T needs --K")
     if args.eps is None:
         raise ValueError("need --eps or --K")
+    if getattr(args, "lut", ""):
+        table = L.load_lut(args.lut)
+        if table.dynamic_range != R:
+            raise RuntimeError(f"LUT was built for R={table.dynamic_range}")
+        q = L.query_lut(table, args.sigma, args.eps)
+        return fbf.fit_fixed_period(samples, q.terms, q.half_period)
     rep = fbf.optimize_parameters(samples, args.eps, fbf.OptimizeOptions(threads=g.threads, device=dev))
     return rep.approximation(R)
 
@@ -171,6 +180,29 @@ def run_compare(args, g) -> int:
     return 0
 
 
+def run_build_lut(args, g) -> int:
+    """fourierbf.cpp:138-158."""
+    sig = [float(v) for v in args.sigmas.split(",") if v]
+    eps = [float(v) for v in args.epsilons.split(",") if v]
+    t0 = time.perf_counter()
+    table = L.build_lut(sig, eps, args.range, args.tmax, g.threads, _device(g))
+    print(f"timing: build {_ms(t0)} ms", file=sys.stderr)
+    L.save_lut(table, args.out)
+    print(f"wrote {table.rows()}x{table.cols()} table to {args.out}")
+    v = L.check_monotone_trends(table)
+    print(f"trend check: {len(v)} deviation(s) from the monotone K*/T* trend")
+    for x in v:
+        print(f"  {x.axis} at sigma-row {x.row}, eps-col {x.col}: {x.detail}")
+    return 0
+
+
+def run_query_lut(args, g) -> int:
+    """fourierbf.cpp:166-172."""
+    q = L.query_lut(L.load_lut(args.lut), args.sigma, args.eps)
+    print(f"K = {q.terms}\nT = {q.half_period}")
+    return 0
+
+
 def parser() -> argparse.ArgumentParser:
     ap = argparse.ArgumentParser(prog="fourierbf-gpu",
                                  description="Bilateral filtering via optimized Fourier range-kernel "
@@ -198,6 +230,7 @@ def parser() -> argparse.ArgumentParser:
     f.add_argument("--method", default="fast", choices=["fast", "brute", "fbf"])
     f.add_argument("--kernel", default="gaussian")
     f.add_argument("--range", type=int, default=255)
+    f.add_argument("--lut", default="", help="lookup table for (K,T) selection")
     c = sub.add_parser("compare", help="run brute and fast, report the error")
     c.add_argument("--in", dest="in_", required=True)
     c.add_argument("--theta", type=float, required=True)
@@ -206,6 +239,16 @@ def parser() -> argparse.ArgumentParser:
     c.add_argument("--report", default="")
     c.add_argument("--kernel", default="gaussian")
     c.add_argument("--range", type=int, default=255)
+    b = sub.add_parser("build-lut", help="tabulate optimal (K*,T*) over a grid")
+    b.add_argument("--sigmas", required=True, help="sigma grid (comma separated)")
+    b.add_argument("--epsilons", required=True, help="eps grid (comma separated)")
+    b.add_argument("--range", type=int, default=255)
+    b.add_argument("--tmax", type=int, default=0)
+    b.add_argument("--out", required=True)
+    q = sub.add_parser("query-lut", help="interpolate (K,T) from a table")
+    q.add_argument("--lut", required=True)
+    q.add_argument("--sigma", type=float, required=True)
+    q.add_argument("--eps", type=float, required=True)
     return ap
 
 
@@ -215,7 +258,8 @@ def main(argv=None) -> int:
         print("error: --threads must be positive", file=sys.stderr)
         return 1
     try:
-        return {"optimize": run_optimize, "filter": run_filter, "compare": run_compare}[args.cmd](args, args)
+        return {"optimize": run_optimize, "filter": run_filter, "compare": run_compare, "build-lut": run_build_lut,
+                "query-lut": run_query_lut}[args.cmd](args, args)
     except (ValueError, RuntimeError, fbf.FbfError) as e:
         print(f"error: {e}", file=sys.stderr)
         return 1

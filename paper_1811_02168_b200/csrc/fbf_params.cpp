@@ -10,6 +10,8 @@
 // 1e-10 * |R_00|, and the minimum-norm solution on the rank-deficient branch.
 // Pinned against the reference's frozen values in tests/test_params.py.
 #include <cmath>
+#include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -561,6 +563,86 @@ int fbf_min_error_over_period_gpu(const double* samples, int R, int K, int t_max
     if (rc != FBF_OK) return rc;
     if (T_best) *T_best = T;
     if (err_out) *err_out = e;
+    clear_error();
+    return FBF_OK;
+}
+
+// lut.cpp:61-113 -- K*, T* per (sigma, eps) cell (Gaussian kernel), row-major
+// [n_sigma][n_eps]; device >= 0 runs the period scans on the GPU (same cells).
+int fbf_build_lut(const double* sigmas, int n_sigma, const double* epsilons, int n_eps, int R, int t_max,
+                  int device, int threads, int* K_out, int* T_out) {
+    if (n_sigma < 2) return fail(FBF_EINVAL, "LUT: sigma grid needs at least two points");
+    for (int i = 1; i < n_sigma; ++i)
+        if (!(sigmas[i] > sigmas[i - 1])) return fail(FBF_EINVAL, "LUT: sigma grid must be strictly ascending");
+    for (int i = 0; i < n_sigma; ++i)
+        if (!(sigmas[i] > 0.0)) return fail(FBF_EINVAL, "LUT: sigma values must be positive");
+    if (n_eps < 2) return fail(FBF_EINVAL, "LUT: eps grid needs at least two points");
+    std::vector<double> logeps(n_eps);
+    for (int j = 0; j < n_eps; ++j) {
+        if (!(epsilons[j] > 0.0) || !(epsilons[j] < 1.0)) return fail(FBF_EINVAL, "LUT: eps values must be in (0, 1)");
+        logeps[j] = std::log10(1.0 / epsilons[j]);
+    }
+    for (int j = 1; j < n_eps; ++j)
+        if (!(logeps[j] > logeps[j - 1]))
+            return fail(FBF_EINVAL, "LUT: log10(1/eps) grid must be strictly ascending");
+    if (R < 1) return fail(FBF_EINVAL, "range kernel: dynamic range must be >= 1");
+    const int cells = n_sigma * n_eps;
+    std::vector<int> status(cells, FBF_OK);
+    std::vector<std::string> msg(cells);
+    auto cell = [&](int c) {
+        const int i = c / n_eps, j = c % n_eps;
+        std::vector<double> b(2 * R + 1), coeffs(2 * R + 1);
+        int rc = fbf_sample_range_kernel(FBF_KERNEL_GAUSSIAN, sigmas[i], R, b.data());
+        ScanBackend be;
+        be.threads = device >= 0 ? std::max(1, threads) : 1;
+        be.device = device;
+        double e = 0.0;
+        if (rc == FBF_OK)
+            rc = optimize_impl(b.data(), R, epsilons[j], t_max, 0, be, &K_out[c], &T_out[c], coeffs.data(),
+                               static_cast<int>(coeffs.size()), &e, nullptr, nullptr);
+        status[c] = rc;
+        if (rc != FBF_OK) msg[c] = last_error_cstr();
+    };
+    if (device >= 0) {
+        for (int c = 0; c < cells; ++c) cell(c);  // one GPU: cells in order, each scan on the device
+    } else {
+        parallel_for(0, cells, threads, cell);   // lut.cpp:87-105
+    }
+    for (int c = 0; c < cells; ++c)
+        if (status[c] != FBF_OK) {
+            char buf[128];
+            std::snprintf(buf, sizeof buf, "LUT build failed at cell sigma=%.17g eps=%.17g: ", sigmas[c / n_eps],
+                          epsilons[c % n_eps]);
+            return fail(status[c] == FBF_EUNREACHABLE ? FBF_EUNREACHABLE : status[c], buf + msg[c]);
+        }
+    clear_error();
+    return FBF_OK;
+}
+
+// lut.cpp:116-143 -- bilinear in (sigma, log10(1/eps)); K rounds up, T to nearest.
+int fbf_query_lut(const double* sigma_grid, int n_sigma, const double* logeps_grid, int n_eps, const int* K,
+                  const int* T, double sigma, double eps, int* K_out, int* T_out) {
+    if (n_sigma < 2 || n_eps < 2) return fail(FBF_EINVAL, "LUT: malformed table");
+    if (!(eps > 0.0) || !(eps < 1.0)) return fail(FBF_ERANGE, "LUT query: eps must be in (0, 1)");
+    const double le = std::log10(1.0 / eps);
+    if (sigma < sigma_grid[0] || sigma > sigma_grid[n_sigma - 1] || le < logeps_grid[0] ||
+        le > logeps_grid[n_eps - 1])
+        return fail(FBF_ERANGE, "LUT query: (sigma, eps) outside the table grid");
+    auto locate = [](const double* g, int n, double x) {
+        const int i = static_cast<int>(std::upper_bound(g, g + n, x) - g);
+        return std::min(i > 0 ? i - 1 : 0, n - 2);
+    };
+    const int i = locate(sigma_grid, n_sigma, sigma), j = locate(logeps_grid, n_eps, le);
+    const double tx = (sigma - sigma_grid[i]) / (sigma_grid[i + 1] - sigma_grid[i]);
+    const double ty = (le - logeps_grid[j]) / (logeps_grid[j + 1] - logeps_grid[j]);
+    auto lerp = [](double a, double b, double t) { return a + t * (b - a); };
+    auto bilinear = [&](const int* g) {
+        const double lo = lerp(g[i * n_eps + j], g[i * n_eps + j + 1], ty);
+        const double hi = lerp(g[(i + 1) * n_eps + j], g[(i + 1) * n_eps + j + 1], ty);
+        return lerp(lo, hi, tx);
+    };
+    *K_out = static_cast<int>(std::ceil(bilinear(K)));
+    *T_out = static_cast<int>(std::lround(bilinear(T)));
     clear_error();
     return FBF_OK;
 }

@@ -239,3 +239,16 @@ def test_cli_filter_compare_optimize(gpu, tmp_path):
     p = _cli("optimize", "--sigma", "50", "--eps", "0.01", "--tmax", "400")
     assert p.returncode == 0, p.stderr
     assert "K* = 4\nT* = 203" in p.stdout
+
+
+def test_cli_lut_commands(gpu, tmp_path):
+    t = tmp_path / "grid.lut"
+    p = _cli("build-lut", "--sigmas", "30,50", "--epsilons", "0.1,0.05", "--tmax", "450", "--out", str(t))
+    assert p.returncode == 0, p.stderr
+    assert "wrote 2x2 table" in p.stdout and "trend check:" in p.stdout
+    p = _cli("query-lut", "--lut", str(t), "--sigma", "50", "--eps", "0.1")
+    assert p.returncode == 0 and p.stdout == "K = 4\nT = 203\n", (p.stdout, p.stderr)
+    p = _cli("filter", "--in", "synth:64x48", "--out", str(tmp_path / "o.pgm"), "--theta", "2", "--sigma", "50",
+             "--eps", "0.1", "--lut", str(t))
+    assert p.returncode == 0, p.stderr
+    assert "params: K=4 T=203" in p.stderr
