@@ -55,6 +55,11 @@ int fbf_device_count(void);
  * its local rank here. */
 int fbf_set_device(int device);
 int fbf_get_device(void);
+/* Page-locked host buffers for the host-buffer entry points (cudaHostAlloc,
+ * portable): pinned memory is what lets H2D/D2H of the pipelined calls run at
+ * the PCIe rate. Pageable buffers work too, at the staged-copy rate. */
+int fbf_host_alloc(size_t bytes, void** ptr);
+int fbf_host_free(void* ptr);
 /* Number of fused-kernel launches this process has issued (all devices). */
 unsigned long long fbf_kernel_launches(void);
 
@@ -149,8 +154,10 @@ int fbf_fast_bilateral_f32_device(const float* d_img, int width, int height, dou
                                   int T, int R, const double* coeffs, int border, float* d_out,
                                   unsigned long long* d_fallbacks, int device, void* stream);
 /* Batch of n_frames independent frames (frame f at img + f*width*height),
- * sharded across the first n_gpus devices (0 -> all), one host thread each.
- * Output frames land in disjoint slices of out. */
+ * sharded across the first n_gpus devices (0 -> all), one host thread each;
+ * n_gpus = 1 uses the default device (fbf_set_device). Within a device the
+ * frames are pipelined: H2D of later frames and D2H of earlier ones overlap
+ * the kernels. Output frames land in disjoint slices of out. */
 int fbf_fast_bilateral_batch_f32(const float* img, int n_frames, int width, int height,
                                  double theta, int K, int T, int R, const double* coeffs,
                                  int border, float* out, long long* fallbacks, int n_gpus);

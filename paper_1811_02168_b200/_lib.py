@@ -35,6 +35,8 @@ SIGNATURES = {
     "fbf_set_device": (_i, [_i]),
     "fbf_get_device": (_i, []),
     "fbf_kernel_launches": (ctypes.c_ulonglong, []),
+    "fbf_host_alloc": (_i, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "fbf_host_free": (_i, [_vp]),
     "fbf_build_spatial_kernel": (_i, [_d, _dp, _i]),
     "fbf_sample_range_kernel": (_i, [_i, _d, _i, _dp]),
     "fbf_frequency_of": (_d, [_i]),

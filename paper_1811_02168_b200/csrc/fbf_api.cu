@@ -691,6 +691,26 @@ int fbf_dev_prof(unsigned long long* out) {
     return 0;
 }
 
+int fbf_host_alloc(size_t bytes, void** ptr) {
+    // page-locked, portable across devices: the copy engines reach ~55 GB/s per
+    // direction from these (measured against ~29 GB/s H2D from some other
+    // pinned allocators, tools/microbench/h2d_probe.cu)
+    *ptr = nullptr;
+    if (bytes == 0) return fail(FBF_EINVAL, "host_alloc: zero bytes");
+    const cudaError_t e = cudaHostAlloc(ptr, bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        *ptr = nullptr;
+        return fail(e == cudaErrorMemoryAllocation ? FBF_ENOMEM : FBF_ECUDA,
+                    std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+    }
+    return FBF_OK;
+}
+
+int fbf_host_free(void* ptr) {
+    if (ptr) FBF_CUDA(cudaFreeHost(ptr), "cudaFreeHost");
+    return FBF_OK;
+}
+
 int fbf_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) {
@@ -800,7 +820,9 @@ int fbf_fast_bilateral_batch_f32(const float* img, int n_frames, int width, int 
     std::vector<long long> fb(G, 0);
     rc = per_device(G, [&](int g) {
         const int f0 = (int)((long long)n_frames * g / G), f1 = (int)((long long)n_frames * (g + 1) / G);
-        return filter_frames_on_device(g, HostIO{img + f0 * fp, out + f0 * fp}, f1 - f0, width, height, theta, a,
+        // one device: the process's default device (fbf_set_device), e.g. its local rank
+        const int dev = G == 1 ? g_default_device.load() : g;
+        return filter_frames_on_device(dev, HostIO{img + f0 * fp, out + f0 * fp}, f1 - f0, width, height, theta, a,
                                        border, &fb[g]);
     });
     if (rc != FBF_OK) return rc;

@@ -166,7 +166,10 @@ struct Geometry {
     static constexpr int RBP = PAIR ? 1 : RBN + 1;
     static constexpr int RROWS = RBP * Q;                        // ring rows per pair
     static constexpr int RS = kTW + 1;                           // ring stride (float2), odd: conflict-free STS.64 across rows
-    static constexpr int NFS = 3;                                // f staging buffers (loader runs ahead)
+#ifndef FBF_NFS
+#define FBF_NFS 3
+#endif
+    static constexpr int NFS = FBF_NFS;                          // f staging buffers (loader runs ahead)
     static constexpr int kMaxBuf = 2;                            // gen / column buffers (named barrier ids)
     static constexpr size_t fstage_bytes = sizeof(float) * NFS * Q * FSW;  // multiple of 128
     static constexpr int n_bars = NFS + 2 * kMaxPairs * RBP;

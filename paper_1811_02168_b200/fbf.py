@@ -435,13 +435,17 @@ def fast_bilateral_u8(img, kernel: SpatialKernel, approx: FourierApproximation,
 
 def fast_bilateral_batch(frames, kernel: SpatialKernel, approx: FourierApproximation,
                          border=BorderPolicy.symmetric, diag: FilterDiagnostics | None = None,
-                         n_gpus: int = 0) -> np.ndarray:
-    """Independent frames (n, height, width), sharded over n_gpus devices (0 = all)."""
+                         n_gpus: int = 0, out: np.ndarray | None = None) -> np.ndarray:
+    """Independent frames (n, height, width), sharded over n_gpus devices (0 = all;
+    1 = the default device), pipelined per device (H2D / kernel / D2H overlap)."""
     a = np.ascontiguousarray(np.asarray(frames), dtype=np.float32)
     if a.ndim != 3:
         raise InvalidArgument("batch: expected (n_frames, height, width)")
     c = _approx_args(approx)
-    out = np.empty_like(a)
+    if out is None:
+        out = np.empty_like(a)
+    elif out.shape != a.shape or out.dtype != np.float32 or not out.flags.c_contiguous:
+        raise InvalidArgument("batch: out must be a C-contiguous float32 array of the input's shape")
     fb = ctypes.c_longlong(0)
     _check(_lib.load().fbf_fast_bilateral_batch_f32(_fptr(a), a.shape[0], a.shape[2], a.shape[1], kernel.theta,
                                                     approx.terms, approx.half_period, approx.dynamic_range,
@@ -528,6 +532,30 @@ def fbf_filter(img, theta: float, sigma: float, eps_or_K: float) -> np.ndarray:
     _check(_lib.load().fbf_filter(_fptr(a), a.shape[0], a.shape[1], float(theta), float(sigma), float(eps_or_K),
                                   _fptr(out)))
     return out
+
+
+class _PinnedBlock:
+    """Owner of one fbf_host_alloc block (freed with the last array view)."""
+
+    def __init__(self, nbytes: int):
+        self.ptr = ctypes.c_void_p(0)
+        _check(_lib.load().fbf_host_alloc(nbytes, ctypes.byref(self.ptr)))
+
+    def __del__(self):
+        if self.ptr and _lib._lib is not None:
+            _lib._lib.fbf_host_free(self.ptr)
+            self.ptr = ctypes.c_void_p(0)
+
+
+def pinned_empty(shape, dtype=np.float32) -> np.ndarray:
+    """numpy array in page-locked host memory (fbf_host_alloc): the host-buffer
+    calls move these over PCIe at the copy-engine rate."""
+    dt = np.dtype(dtype)
+    n = int(np.prod(shape)) * dt.itemsize
+    blk = _PinnedBlock(max(n, 1))
+    buf = (ctypes.c_char * max(n, 1)).from_address(blk.ptr.value)
+    buf._fbf_owner = blk  # keeps the block alive as long as any view of buf
+    return np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape)
 
 
 # ---- brute filter and metrics (filter.cpp:83-127, metrics.hpp) --------------
