@@ -82,6 +82,17 @@ constexpr size_t kSmemReservedPerBlock = 1024;
 //               the sub-partitions so that each gets the same FFMA2 work
 //               (Params::warp_role), for up to 7 pairs per launch.
 constexpr int kPairMode = 0, kSplitMode = 1, kHalfMode = 2;
+// Pair mode with 7 pairs (16 warps): warpgroups 2-3 (7 pair warps + loader) run at
+// FBF_REGSPLIT_HI registers, warpgroups 0-1 (gen + combine) at FBF_REGSPLIT_LO
+// (setmaxnreg; 8 x LO + 8 x HI = 16 x 128). Measured on c1: 96/160 0.571 of the
+// FMA peak vs 0.550 with the single 128-register layout (FBF_NO_REGSPLIT).
+#ifndef FBF_REGSPLIT_LO
+#define FBF_REGSPLIT_LO 96
+#endif
+#ifndef FBF_REGSPLIT_HI
+#define FBF_REGSPLIT_HI 160
+#endif
+static_assert(FBF_REGSPLIT_LO + FBF_REGSPLIT_HI == 256, "8 warps at LO + 8 at HI must equal 16 warps at 128");
 constexpr int kHalfMaxPairs = 7;
 // threads of a launch: FFMA2 warps, plus combine, gen and loader (half mode:
 // rounded up to whole sub-partition rows, unused slots idle)
@@ -321,6 +332,7 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 #endif
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ int lane_id_() { return (int)(threadIdx.x & 31); }
 // barrier ids (0 is __syncthreads): gen full/empty, column full/empty, f stage empty
 constexpr int kBarGenFull = 1, kBarGenEmpty = 3, kBarColFull = 5, kBarColEmpty = 7, kBarFsEmpty = 9;
 
@@ -497,6 +509,17 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
         else if (t < nf + kCombThreads)    { role = kRoleComb; tid = t - nf; }
         else if (t < nf + CG)              { role = kRoleGen; tid = t - nf - kCombThreads; }
         else                               { role = kRoleLoad; tid = t - nf - CG; }
+#ifndef FBF_NO_REGSPLIT
+        // register-split layout (pair mode, 7 pairs, 16 warps): warpgroups 2-3 hold the
+        // 7 pair warps and the loader, 0-1 the combine and gen warps, so that every
+        // role's code runs from one instance only (no duplicated hot code)
+        if (M == kPairMode && NKR == 3 && blockDim.x == 512 && np == 7 && t >= nf) {
+            const int w = (int)(threadIdx.x / 32);  // 0..8
+            if (w == 8)     { role = kRoleLoad; tid = lane_id_(); }
+            else if (w >= 4) { role = kRoleComb; tid = (7 - w) * 32 + lane_id_(); }
+            else            { role = kRoleGen; tid = (3 - w) * 32 + lane_id_(); }
+        }
+#endif
     }
     const int lane = threadIdx.x & 31;
     const int zk = p.k_lo == 0 ? 1 : 0;  // k = 0 contributes the single pair (f, 1)
@@ -984,7 +1007,28 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
 #ifdef FBF_DEV_PAIRONLY
     if (role != kRoleRow) role = kRoleIdle;
 #endif
+#ifndef FBF_NO_REGSPLIT
+    // Register split between warpgroups (pair mode, 7 pairs, 16 warps): warpgroups
+    // 0-1 (loader, gen, 3 combine warps) give up registers, 2-3 (7 pair warps +
+    // one combine warp) take them, so the pair warps' row pass can keep loads in
+    // flight next to the 2r live column partial sums. 8 x 96 + 8 x 160 = 16 x 128.
+    if constexpr (M == kPairMode && NKR == 3) {
+        if (blockDim.x == 512 && np == 7) {
+            if (threadIdx.x < 256) {
+                asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(FBF_REGSPLIT_LO));
+                if (role != kRoleIdle) run_roles(std::false_type{});
+            } else {
+                asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(FBF_REGSPLIT_HI));
+                run_roles(std::true_type{});
+            }
+            goto roles_done;
+        }
+    }
+#endif
     if (role != kRoleIdle) run_roles(std::true_type{});
+#ifndef FBF_NO_REGSPLIT
+roles_done:
+#endif
     if (role == kRoleComb && p.fallbacks) {
         const unsigned w = __reduce_add_sync(0xffffffffu, n_fallbacks);
         if (lane == 0 && w) atomicAdd(p.fallbacks, (unsigned long long)w);
