@@ -145,25 +145,37 @@ def cpu_reference_run(img, cfg, approx, seconds: float, min_reps: int = 1):
     return kind, threads, times
 
 
+def cpu_sample(cfg, img):
+    """The bounded CPU-reference sample of a config: the image (c0-c2), one frame
+    (c3), or the first 1024 rows of the 16384x16384 image (c4: the full image
+    takes ~100 s on 8 cores)."""
+    if cfg.sharding == "bands" and img.shape[0] > 1024:
+        return img[:1024], f"rows [0, 1024) of the {cfg.width}x{cfg.height} image"
+    if cfg.sharding == "frames":
+        return img, f"frame 0 of the {cfg.frames}-frame {cfg.width}x{cfg.height} batch"
+    return img, f"full {cfg.width}x{cfg.height} image"
+
+
 def run_reference_impl(args, cfg):
     rank, world, local = dist_env()
     if rank != 0:
         return
     from paper_1811_02168_b200 import configs
-    img = configs.make_frame(cfg, 0)
+    img, sample = cpu_sample(cfg, configs.make_frame(cfg, 0))
     approx = configs.select(cfg)
     _, _, wt = cpu_reference_run(img, cfg, approx, 0.0, min_reps=max(0, args.warmup))
     kind, threads, times = cpu_reference_run(img, cfg, approx, 0.0, min_reps=args.steps)
     total = sum(times)
-    mp = cfg.width * cfg.height * len(times) / total / 1e6
+    mp = img.size * len(times) / total / 1e6
     line = {
         "metric": "megapixels_per_sec", "value": round(mp, 4), "unit": "MP/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "weak" if cfg.sharding == "single" else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.width}x{cfg.height} {cfg.generator} image, theta={cfg.theta}, "
                                f"sigma={cfg.sigma}, K={approx.terms}, T={approx.half_period}, symmetric border"},
         "cpu_baseline": {"value": round(mp, 4), "unit": "MP/s", "cores": threads, "kind": kind,
-                         "sample": f"one full {cfg.width}x{cfg.height} image per step"},
+                         "sample": f"{sample} per step, fp64 fast_bilateral"},
         "e2e": {"value": round(mp, 4), "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -181,7 +193,7 @@ def main():
     import numpy as np
     import torch
     import paper_1811_02168_b200 as fb
-    from paper_1811_02168_b200 import _lib
+    from paper_1811_02168_b200 import _lib, shard
 
     lib = _lib.load()
     torch.cuda.set_device(local)
@@ -197,24 +209,65 @@ def main():
             import torch.distributed as dist
             dist.barrier()
 
-    # per-rank independent image (frame `rank` of the config's generator)
-    img = configs.make_frame(cfg, rank)
+    def max_ranks(*vals):
+        t = torch.tensor(list(vals), dtype=torch.float64, device=dev)
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(v) for v in t.tolist()]
+
+    # Work of this rank (no collective on the data path):
+    #   single (c0-c2): every rank filters its own image (frame `rank`)   -> weak scaling
+    #   frames (c3): the cfg.frames frames in contiguous blocks per rank   -> strong scaling
+    #   bands  (c4): one image, a row band + replicated halo per rank     -> strong scaling
+    mode = cfg.sharding
     approx = configs.select(cfg)
     kernel = fb.build_spatial_kernel(cfg.theta)
-    H, W = img.shape
-    pixels = H * W
+    H, W = cfg.height, cfg.width
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(dev)
-    d_in = torch.from_numpy(img).to(dev)
-    d_out = torch.empty_like(d_in)
+    if mode == "frames":
+        f0, f1 = shard.frame_range(cfg.frames, rank, world)
+        frames = np.stack([configs.make_frame(cfg, f) for f in range(f0, f1)])
+        local_px, total_px = frames.size, cfg.frames * H * W
+        img0 = frames[0]
+        d_in = torch.from_numpy(frames).to(dev)
+        d_out = torch.empty_like(d_in)
+        work = f"frames [{f0}, {f1}) of {cfg.frames} on this rank"
+    elif mode == "bands":
+        full = configs.make_frame(cfg, 0)
+        band = shard.band_for_rank(H, rank, world, cfg.theta)
+        src = np.ascontiguousarray(full[band.src_row0:band.src_row0 + band.src_rows])
+        local_px, total_px = band.out_rows * W, H * W
+        img0 = full
+        d_in = torch.from_numpy(src).to(dev)
+        d_out = torch.empty((band.out_rows, W), dtype=torch.float32, device=dev)
+        work = (f"output rows [{band.out_row0}, {band.out_row0 + band.out_rows}) + halo rows "
+                f"[{band.src_row0}, {band.src_row0 + band.src_rows}) on this rank")
+    else:
+        img0 = configs.make_frame(cfg, rank)
+        local_px, total_px = img0.size, world * img0.size
+        d_in = torch.from_numpy(img0).to(dev)
+        d_out = torch.empty_like(d_in)
+        work = "one image per rank"
     d_fb = torch.zeros(1, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     fb.validate_device(d_in)
 
+    def step():
+        if mode == "frames":
+            for i in range(d_in.shape[0]):
+                fb.fast_bilateral_device(d_in[i], kernel, approx, d_out[i], d_fallbacks=d_fb, stream=stream)
+        elif mode == "bands":
+            fb.fast_bilateral_band_device(d_in, band.src_row0, H, band.out_row0, band.out_rows, kernel, approx,
+                                          d_out, d_fallbacks=d_fb, stream=stream)
+        else:
+            fb.fast_bilateral_device(d_in, kernel, approx, d_out, d_fallbacks=d_fb, stream=stream)
+
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             flush.zero_()
-            fb.fast_bilateral_device(d_in, kernel, approx, d_out, d_fallbacks=d_fb, stream=stream)
+            step()
     torch.cuda.synchronize(dev)
     barrier()
     torch.cuda.synchronize(dev)
@@ -225,67 +278,121 @@ def main():
             for s in range(args.steps):
                 flush.zero_()
                 ev[s][0].record(stream)
-                fb.fast_bilateral_device(d_in, kernel, approx, d_out, d_fallbacks=d_fb, stream=stream)
+                step()
                 ev[s][1].record(stream)
         torch.cuda.synchronize(dev)
     launches = lib.fbf_kernel_launches() - launches0
     barrier()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        import torch.distributed as dist
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms_max = float(t.item())
-    value = world * pixels * args.steps / (total_ms_max * 1e-3) / 1e6
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    total_ms_max, = max_ranks(total_ms)
+    value = total_px * args.steps / (total_ms_max * 1e-3) / 1e6
+    if mode == "single":
+        value = world * local_px * args.steps / (total_ms_max * 1e-3) / 1e6
 
     # ---- e2e through the host-buffer public API (pinned H2D + D2H inside) ----
-    # (1) one fast_bilateral call per step (latency-bound: band pipeline inside the call)
-    a_in = fb.pinned_empty(img.shape)
-    a_in[:] = img
-    a_out = fb.pinned_empty(img.shape)
-    for _ in range(max(3, args.warmup)):
-        fb.fast_bilateral(a_in, kernel, approx, out=a_out)
-    barrier()
-    e2e_times = []
     diag = fb.FilterDiagnostics()
-    for _ in range(args.e2e_steps):
-        t0 = time.perf_counter()
-        fb.fast_bilateral(a_in, kernel, approx, diag=diag, out=a_out)
-        e2e_times.append(time.perf_counter() - t0)
-    print(f"e2e single-call step ms: {' '.join(f'{1e3 * x:.3f}' for x in e2e_times)}", file=sys.stderr)
-    # (2) the same steps as frames of fast_bilateral_batch calls on this rank's device:
-    # H2D of the next frames and D2H of the previous ones overlap each frame's kernel
-    n_batch = max(1, min(args.e2e_steps, (512 << 20) // (pixels * 4)))
-    e2e_batch_times = []
-    if n_batch >= 2:
-        b_in = fb.pinned_empty((n_batch,) + img.shape)
-        b_in[:] = img
-        b_out = fb.pinned_empty((n_batch,) + img.shape)
+    e2e_calls, api = [], ""
+    h2d_step = d2h_step = 0
+    if mode == "single":
+        # (1) one fast_bilateral call per step (band pipeline inside the call)
+        a_in = fb.pinned_empty(img0.shape)
+        a_in[:] = img0
+        a_out = fb.pinned_empty(img0.shape)
+        for _ in range(max(3, args.warmup)):
+            fb.fast_bilateral(a_in, kernel, approx, out=a_out)
+        barrier()
+        single_times = []
+        for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
+            fb.fast_bilateral(a_in, kernel, approx, diag=diag, out=a_out)
+            single_times.append(time.perf_counter() - t0)
+        print(f"e2e single-call step ms: {' '.join(f'{1e3 * x:.3f}' for x in single_times)}", file=sys.stderr)
+        # (2) the same steps as frames of fast_bilateral_batch calls on this rank's device:
+        # H2D of the next frames and D2H of the previous ones overlap each frame's kernel
+        n_batch = max(1, min(args.e2e_steps, (512 << 20) // (img0.size * 4)))
+        if n_batch >= 2:
+            b_in = fb.pinned_empty((n_batch,) + img0.shape)
+            b_in[:] = img0
+            b_out = fb.pinned_empty((n_batch,) + img0.shape)
+            fb.fast_bilateral_batch(b_in, kernel, approx, out=b_out, n_gpus=1)
+            barrier()
+            done = 0
+            while done < args.e2e_steps or len(e2e_calls) < 3:
+                t0 = time.perf_counter()
+                fb.fast_bilateral_batch(b_in, kernel, approx, diag=diag, out=b_out, n_gpus=1)
+                e2e_calls.append((time.perf_counter() - t0, n_batch))
+                done += n_batch
+            print(f"e2e batch ({n_batch} frames) call ms: {' '.join(f'{1e3 * x:.3f}' for x, _ in e2e_calls)}",
+                  file=sys.stderr)
+            api = (f"fbf_fast_bilateral_batch_f32, {n_batch} steps (frames) per call from pinned host buffers: "
+                   "H2D/kernel/D2H pipelined across frames")
+        else:
+            e2e_calls = [(x, 1) for x in single_times]
+            api = "fbf_fast_bilateral_f32, one call per step from pinned host buffers"
+        single_total, = max_ranks(sum(single_times))
+        single_value = world * local_px * args.e2e_steps / single_total / 1e6
+        h2d_step, d2h_step = img0.size * 4, img0.size * 4 + 16
+    elif mode == "frames":
+        # one fast_bilateral_batch call per step over this rank's frames (pipelined)
+        b_in = fb.pinned_empty(frames.shape)
+        b_in[:] = frames
+        b_out = fb.pinned_empty(frames.shape)
         fb.fast_bilateral_batch(b_in, kernel, approx, out=b_out, n_gpus=1)
         barrier()
-        done = 0
-        while done < args.e2e_steps or len(e2e_batch_times) < 3:
+        for _ in range(max(3, min(args.e2e_steps, 5))):
             t0 = time.perf_counter()
             fb.fast_bilateral_batch(b_in, kernel, approx, diag=diag, out=b_out, n_gpus=1)
-            e2e_batch_times.append(time.perf_counter() - t0)
-            done += n_batch
-        print(f"e2e batch ({n_batch} frames) call ms: {' '.join(f'{1e3 * x:.3f}' for x in e2e_batch_times)}",
-              file=sys.stderr)
+            e2e_calls.append((time.perf_counter() - t0, 1))
+        api = "fbf_fast_bilateral_batch_f32 over the rank's frames per step, pinned host buffers, pipelined"
+        h2d_step, d2h_step = frames.size * 4, frames.size * 4 + 16
+        single_value = None
+    else:
+        if world == 1:
+            # the whole image through the public single-image call (8 pipelined row bands)
+            a_in = fb.pinned_empty(full.shape)
+            a_in[:] = full
+            a_out = fb.pinned_empty(full.shape)
+            fb.fast_bilateral(a_in, kernel, approx, out=a_out)
+            for _ in range(max(2, min(args.e2e_steps, 3))):
+                t0 = time.perf_counter()
+                fb.fast_bilateral(a_in, kernel, approx, diag=diag, out=a_out)
+                e2e_calls.append((time.perf_counter() - t0, 1))
+            api = "fbf_fast_bilateral_f32 on the whole image (row bands pipelined inside the call), pinned buffers"
+            h2d_step, d2h_step = full.size * 4, full.size * 4 + 16
+        else:
+            # this rank's halo window H2D, the band entry point, the band D2H
+            h_src = fb.pinned_empty(src.shape)
+            h_src[:] = src
+            h_dst = fb.pinned_empty((band.out_rows, W))
+            t_src, t_dst = torch.from_numpy(h_src), torch.from_numpy(h_dst)
+
+            def e2e_band():
+                with torch.cuda.stream(stream):
+                    d_in.copy_(t_src, non_blocking=True)
+                    fb.fast_bilateral_band_device(d_in, band.src_row0, H, band.out_row0, band.out_rows, kernel,
+                                                  approx, d_out, d_fallbacks=d_fb, stream=stream)
+                    t_dst.copy_(d_out, non_blocking=True)
+                stream.synchronize()
+
+            e2e_band()
+            barrier()
+            for _ in range(max(2, min(args.e2e_steps, 3))):
+                t0 = time.perf_counter()
+                e2e_band()
+                e2e_calls.append((time.perf_counter() - t0, 1))
+            api = "fbf_fast_bilateral_band_f32_device with the rank's halo window H2D and band D2H (pinned)"
+            h2d_step, d2h_step = src.size * 4, band.out_rows * W * 4
+        single_value = None
     barrier()
-    e2e_total = torch.tensor([sum(e2e_times), sum(e2e_batch_times)], dtype=torch.float64, device=dev)
-    if world > 1:
-        import torch.distributed as dist
-        dist.all_reduce(e2e_total, op=dist.ReduceOp.MAX)
-    e2e_single = world * pixels * args.e2e_steps / float(e2e_total[0].item()) / 1e6
-    e2e_batch = (world * pixels * n_batch * len(e2e_batch_times) / float(e2e_total[1].item()) / 1e6
-                 if e2e_batch_times else None)
-    e2e_value = e2e_batch if e2e_batch is not None else e2e_single
+    e2e_total, = max_ranks(sum(t for t, _ in e2e_calls))
+    e2e_units = sum(n for _, n in e2e_calls)
+    e2e_value = (world * local_px if mode == "single" else total_px) * e2e_units / e2e_total / 1e6
 
     if rank == 0:
         flop_px = cfg.flop_per_pixel(approx.terms)
-        mean_launch_s = (total_ms / args.steps) * 1e-3 / max(1, launches // max(1, args.steps))
-        per_launch_flop = flop_px * pixels / max(1, launches // max(1, args.steps))
+        per_step = max(1, launches // max(1, args.steps))
+        mean_launch_s = (total_ms / args.steps) * 1e-3 / per_step
+        per_launch_flop = flop_px * local_px / per_step
         achieved = per_launch_flop / mean_launch_s / 1e12
         n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
         peaks = measured_peaks()
@@ -296,23 +403,28 @@ def main():
         if os.path.exists(prof):
             with open(prof) as f:
                 traffic = json.load(f).get(cfg.name)
+        e2e = {"value": round(e2e_value, 2), "unit": "MP/s", "h2d_bytes_per_step": h2d_step,
+               "d2h_bytes_per_step": d2h_step, "api": api}
+        if single_value is not None:
+            e2e["single_call_value"] = round(single_value, 2)
+        shards = {"single": f"frames one-per-GPU x{world}, no collective",
+                  "frames": f"{cfg.frames} frames in contiguous blocks over {world} GPU(s), no collective",
+                  "bands": f"row bands with replicated {cfg.radius}-row halos over {world} GPU(s), no collective"}
         line = {
             "metric": "megapixels_per_sec", "value": round(value, 2), "unit": "MP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms_max / args.steps, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": f"synthetic ({cfg.generator}, {cfg.sites} sites, noise {cfg.noise}, seed {cfg.frame_seed(rank)}+rank)",
-            "config": {"workload": f"{cfg.name}: {W}x{H} image per GPU, theta={cfg.theta} (r={cfg.radius}), "
-                                   f"sigma={cfg.sigma}, K={approx.terms}, T={approx.half_period}, "
-                                   f"{4 * approx.terms - 2} channels, symmetric border",
+            "higher_is_better": True, "scaling": "weak" if mode == "single" else "strong", "vs_baseline": None,
+            "dtype": "f32",
+            "data": f"synthetic ({cfg.generator}, {cfg.sites} sites, noise {cfg.noise}, seed {cfg.frame_seed(0)}"
+                    + ("+rank)" if mode == "single" else "+frame)" if mode == "frames" else ")"),
+            "config": {"workload": f"{cfg.name}: {W}x{H}" + (f" x{cfg.frames} frames" if mode == "frames" else "")
+                                   + f" image{' per GPU' if mode == 'single' else ''}, theta={cfg.theta} "
+                                     f"(r={cfg.radius}), sigma={cfg.sigma}, K={approx.terms}, T={approx.half_period}, "
+                                     f"{4 * approx.terms - 2} channels, symmetric border; rank 0: {work}",
                        "l2": "256 MiB memset flush between timed steps (outside the events)",
-                       "parallelism": f"frames one-per-GPU x{world}, no collective"},
+                       "parallelism": shards[mode]},
             "gpu_launches": int(launches),
-            "e2e": {"value": round(e2e_value, 2), "unit": "MP/s", "h2d_bytes_per_step": pixels * 4,
-                    "d2h_bytes_per_step": pixels * 4 + 16,
-                    "api": (f"fbf_fast_bilateral_batch_f32, {n_batch} steps (frames) per call from pinned host "
-                            "buffers: H2D/kernel/D2H pipelined across frames" if e2e_batch is not None else
-                            "fbf_fast_bilateral_f32, one call per step from pinned host buffers"),
-                    "single_call_value": round(e2e_single, 2)},
+            "e2e": e2e,
             "roofline": {"bound": "fp32-fma", "achieved": round(achieved, 3), "peak": round(peak, 2),
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "flop_per_pixel": flop_px,
@@ -322,10 +434,11 @@ def main():
             "fallback_pixels": int(diag.fallback_pixels),
         }
         if world == 1 and not args.no_cpu_baseline:
-            kind, threads, times = cpu_reference_run(img, cfg, approx, args.cpu_seconds)
-            mp = pixels * len(times) / sum(times) / 1e6
+            sample_img, sample = cpu_sample(cfg, img0)
+            kind, threads, times = cpu_reference_run(sample_img, cfg, approx, args.cpu_seconds)
+            mp = sample_img.size * len(times) / sum(times) / 1e6
             line["cpu_baseline"] = {"value": round(mp, 4), "unit": "MP/s", "cores": threads, "kind": kind,
-                                    "sample": f"{len(times)} x full {W}x{H} image, fp64 fast_bilateral"}
+                                    "sample": f"{len(times)} x {sample}, fp64 fast_bilateral"}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
