@@ -256,8 +256,7 @@ def main():
 
     def step():
         if mode == "frames":
-            for i in range(d_in.shape[0]):
-                fb.fast_bilateral_device(d_in[i], kernel, approx, d_out[i], d_fallbacks=d_fb, stream=stream)
+            fb.fast_bilateral_batch_device(d_in, kernel, approx, d_out, d_fallbacks=d_fb, stream=stream)
         elif mode == "bands":
             fb.fast_bilateral_band_device(d_in, band.src_row0, H, band.out_row0, band.out_rows, kernel, approx,
                                           d_out, d_fallbacks=d_fb, stream=stream)

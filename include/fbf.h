@@ -177,6 +177,12 @@ int fbf_fast_bilateral_band_f32_device(const float* d_src, int src_row0, int src
                                        double theta, int K, int T, int R, const double* coeffs,
                                        int border, float* d_dst,
                                        unsigned long long* d_fallbacks, int device, void* stream);
+/* Device-resident batch: n_frames frames at d_img + f*width*height, one
+ * launch on `stream` (CTAs share the (frame, strip, row) units evenly, so the
+ * per-segment warm-up rows amortise over the batch). No validation. */
+int fbf_fast_bilateral_batch_f32_device(const float* d_img, int n_frames, int width, int height, double theta, int K,
+                                        int T, int R, const double* coeffs, int border, float* d_out,
+                                        unsigned long long* d_fallbacks, int device, void* stream);
 /* Global source-row window [*row0, *row0 + *rows) needed for output rows
  * [out_row0, out_row0 + out_rows) at radius ceil(3 theta). */
 int fbf_band_source_rows(int height, int out_row0, int out_rows, double theta, int border,

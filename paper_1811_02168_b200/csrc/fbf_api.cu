@@ -794,6 +794,37 @@ int fbf_fast_bilateral_band_f32_device(const float* d_src, int src_row0, int src
     return rc;
 }
 
+int fbf_fast_bilateral_batch_f32_device(const float* d_img, int n_frames, int width, int height, double theta, int K,
+                                        int T, int R, const double* coeffs, int border, float* d_out,
+                                        unsigned long long* d_fallbacks, int device, void* stream) {
+    int r = 0;
+    int rc = check_args(width, height, theta, K, T, R, coeffs, border, &r);
+    if (rc != FBF_OK) return rc;
+    if (n_frames <= 0) return fail(FBF_EINVAL, "batch: n_frames must be positive");
+    Approx a;
+    rc = make_approx(K, T, R, coeffs, a);
+    if (rc != FBF_OK) return rc;
+    DeviceCtx* ctx = nullptr;
+    rc = get_ctx(device, &ctx);
+    if (rc != FBF_OK) return rc;
+    std::lock_guard<std::mutex> lock(ctx->mtx);
+    FBF_CUDA(cudaSetDevice(device), "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t fp = (size_t)width * height;
+    const size_t scr = scratch_bytes(a, theta, (size_t)n_frames * fp);
+    float2* d_scr = nullptr;
+    if (scr) {
+        rc = ctx->reserve(scr);
+        if (rc != FBF_OK) return rc;
+        d_scr = (float2*)ctx->arena;
+    }
+    // one launch over all frames: CTAs take contiguous (frame, strip, row) shares
+    Job job{d_img, (long long)fp, 0, height, d_out, (long long)fp, width, height, n_frames, 0, height};
+    rc = run_job(*ctx, job, theta, a, border, d_scr, d_fallbacks, st);
+    if (rc == FBF_OK) clear_error();
+    return rc;
+}
+
 int fbf_band_source_rows(int height, int out_row0, int out_rows, double theta, int border, int* row0,
                          int* rows) {
     if (!(theta > 0.0) || height <= 0 || out_rows <= 0 || out_row0 < 0 || out_row0 + out_rows > height)

@@ -501,6 +501,22 @@ def fast_bilateral_device(d_img, kernel: SpatialKernel, approx: FourierApproxima
         ctypes.c_void_p(st.cuda_stream)))
 
 
+def fast_bilateral_batch_device(d_frames, kernel: SpatialKernel, approx: FourierApproximation, d_out,
+                                border=BorderPolicy.symmetric, d_fallbacks=None, stream=None) -> None:
+    """Device-resident batch (n_frames, H, W) float32 CUDA tensors, one launch."""
+    import torch
+    if d_frames.dtype != torch.float32 or not d_frames.is_cuda or not d_frames.is_contiguous() or d_frames.dim() != 3:
+        raise InvalidArgument("device frames must be a contiguous (n, H, W) float32 CUDA tensor")
+    n, H, W = d_frames.shape
+    c = _approx_args(approx)
+    st = stream if stream is not None else torch.cuda.current_stream(d_frames.device)
+    _check(_lib.load().fbf_fast_bilateral_batch_f32_device(
+        ctypes.c_void_p(d_frames.data_ptr()), n, W, H, kernel.theta, approx.terms, approx.half_period,
+        approx.dynamic_range, _dptr(c), _border(border), ctypes.c_void_p(d_out.data_ptr()),
+        ctypes.c_void_p(d_fallbacks.data_ptr() if d_fallbacks is not None else 0), d_frames.device.index,
+        ctypes.c_void_p(st.cuda_stream)))
+
+
 def fast_bilateral_band_device(d_src, src_row0: int, height: int, out_row0: int, out_rows: int,
                                kernel: SpatialKernel, approx: FourierApproximation, d_dst,
                                border=BorderPolicy.symmetric, d_fallbacks=None, stream=None) -> None:

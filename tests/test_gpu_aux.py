@@ -252,3 +252,20 @@ def test_cli_lut_commands(gpu, tmp_path):
              "--eps", "0.1", "--lut", str(t))
     assert p.returncode == 0, p.stderr
     assert "params: K=4 T=203" in p.stderr
+
+
+def test_device_batch_equals_per_frame(gpu):
+    # one launch over all frames == one launch per frame, bit for bit
+    import torch
+    fb = gpu
+    frames = np.stack([fb.voronoi_image(300, 170, 16, 10.0, 77 + f) for f in range(5)])
+    k = fb.build_spatial_kernel(5.0)
+    for a in (fb.select_parameters(30.0, eps=0.1), fb.select_parameters(15.0, eps=0.01)):  # 1 and 2 chunks
+        d = torch.from_numpy(frames).cuda()
+        o = torch.empty_like(d)
+        fb.fast_bilateral_batch_device(d, k, a, o)
+        per = torch.empty_like(d)
+        for i in range(d.shape[0]):
+            fb.fast_bilateral_device(d[i], k, a, per[i])
+        torch.cuda.synchronize()
+        assert torch.equal(o, per)
