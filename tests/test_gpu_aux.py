@@ -269,3 +269,15 @@ def test_device_batch_equals_per_frame(gpu):
             fb.fast_bilateral_device(d[i], k, a, per[i])
         torch.cuda.synchronize()
         assert torch.equal(o, per)
+
+
+def test_gpu_brute_large_range_lattice(gpu, ref_lib):
+    # 2R+1 > 4096: the range lattice is read from global memory instead of shared
+    fb = gpu
+    R = 3000
+    rs = np.random.default_rng(9)
+    img = np.round(rs.uniform(0, R, (40, 53))).astype(np.float32)
+    rng = ref_lib.range_samples("gaussian", 400.0, R)
+    ref, ref_fb = ref_lib.brute_bilateral(img.astype(np.float64), 2.0, rng, R=R)
+    out = fb.brute_bilateral(img, fb.build_spatial_kernel(2.0), fb.RangeKernelSamples(R, rng))
+    assert np.array_equal(out, ref)
