@@ -163,6 +163,7 @@ struct Geometry {
     static constexpr bool PAIR = M == kPairMode;
     static constexpr int GW = kTW + 2 * R;                       // gen row width (pixels)
     static constexpr int GS = GW + ((2 - GW % 4) + 4) % 4;       // gen stride (float2), GS/2 odd
+    static_assert(GS % 2 == 0, "gen pixel pairs are stored with 16-byte STS");
     static constexpr int FSW = (GW + 3 + 3) / 4 * 4;             // f staging row: GW + 16B-alignment slack
     // Column pass form: for R <= kScatterMaxRadius the 2R partial sums of a column
     // live in registers ("scatter": every row-pass output is read once), so the
@@ -260,6 +261,12 @@ __device__ __forceinline__ void sts2(float2* p, float2 v) {
     // volatile keeps the order against the (volatile) barrier instructions that
     // publish the data; no memory clobber, so loads and math still schedule freely
     asm volatile("st.shared.v2.f32 [%0], {%1, %2};\n" ::"r"((unsigned)__cvta_generic_to_shared(p)), "f"(v.x), "f"(v.y));
+}
+
+// two adjacent float2 (16-byte aligned) as one st.shared.v4.f32
+__device__ __forceinline__ void sts4(float2* p, float2 a, float2 b) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"((unsigned)__cvta_generic_to_shared(p)),
+                 "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
 }
 
 // 1/x to ~1 ulp (MUFU.RCP); out = num / den has the same tolerance budget as
@@ -603,45 +610,60 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
         const unsigned nrows = (unsigned)max(hi - lo, 0);
         const float inv = p.inv_period;
         const bool kfirst = p.k_first > 1;
+        // MASKED: zero border -- pixels outside the image and rows outside the needed
+        // window contribute exact zeros. Symmetric / replicate borders map every staged
+        // pixel into the image, and rows outside [lo, hi) (stale stage data) only reach
+        // output rows that are never stored: each output's column sum opens fresh R rows
+        // above it (col_scatter) and the combine writes rows [ya, yb) only -- so the
+        // unmasked body skips the selects.
+        auto body = [&](auto masked_c) {
+            constexpr bool MASKED = decltype(masked_c)::value;
 #pragma unroll 2
-        for (int it = 0; it < GITER; ++it) {
-            const int q = gi[it].q;
-            if (q >= 0) {
-                // unconditional loads (rows the loader skipped hold stale values), then select
-                const float fa = fs[gi[it].fso], fbv = fs[gi[it].fso + 1];
-                const bool rowok = (unsigned)(a + q - lo) < nrows;
-                const bool va = rowok && (gi[it].cm & 1), vb = rowok && (gi[it].cm & 2);
-                const float2 f = make_float2(va ? fa : 0.f, vb ? fbv : 0.f);
-                // per pixel (first, second) channel pairs, stored as float2 at gp[0] / gp[1]
-                float2* gp = gbuf + gi[it].go;
-                if (zk) {
-                    sts2(gp, make_float2(f.x, va ? 1.f : 0.f));
-                    sts2(gp + 1, make_float2(f.y, vb ? 1.f : 0.f));
-                }
-                if (NKR > 0) {
-                    const CS2 h = harmonic1x2(f, inv);
-                    const float2 w0 = make_float2(h.c.x, h.s.x), w1 = make_float2(h.c.y, h.s.y);
-                    float2 z0 = kfirst ? harmonic_first1(w0, p.k_first) : w0;
-                    float2 z1 = kfirst ? harmonic_first1(w1, p.k_first) : w1;
-                    if (!va) z0 = make_float2(0.f, 0.f);
-                    if (!vb) z1 = make_float2(0.f, 0.f);
-                    float2* gk = gp + zk * (Q * GS);
+            for (int it = 0; it < GITER; ++it) {
+                const int q = gi[it].q;
+                if (q >= 0) {
+                    // unconditional loads (rows the loader skipped hold stale values), then select
+                    const float fa = fs[gi[it].fso], fbv = fs[gi[it].fso + 1];
+                    bool va = true, vb = true;
+                    if constexpr (MASKED) {
+                        const bool rowok = (unsigned)(a + q - lo) < nrows;
+                        va = rowok && (gi[it].cm & 1);
+                        vb = rowok && (gi[it].cm & 2);
+                    }
+                    const float2 f = MASKED ? make_float2(va ? fa : 0.f, vb ? fbv : 0.f) : make_float2(fa, fbv);
+                    // per pixel (first, second) channel pairs, stored as float2 at gp[0] / gp[1]
+                    float2* gp = gbuf + gi[it].go;
+                    if (zk) {
+                        sts4(gp, make_float2(f.x, MASKED && !va ? 0.f : 1.f), make_float2(f.y, MASKED && !vb ? 0.f : 1.f));
+                    }
+                    if (NKR > 0) {
+                        const CS2 h = harmonic1x2(f, inv);
+                        const float2 w0 = make_float2(h.c.x, h.s.x), w1 = make_float2(h.c.y, h.s.y);
+                        float2 z0 = kfirst ? harmonic_first1(w0, p.k_first) : w0;
+                        float2 z1 = kfirst ? harmonic_first1(w1, p.k_first) : w1;
+                        if constexpr (MASKED) {
+                            if (!va) z0 = make_float2(0.f, 0.f);
+                            if (!vb) z1 = make_float2(0.f, 0.f);
+                        }
+                        float2* gk = gp + zk * (Q * GS);
 #pragma unroll
-                    for (int kk = 0; kk < NKR; ++kk) {
-                        float2* pf = gk + (2 * kk) * (Q * GS);      // (C_k f, S_k f)
-                        float2* pc = gk + (2 * kk + 1) * (Q * GS);  // (C_k, S_k)
-                        sts2(pf, __fmul2_rn(z0, make_float2(f.x, f.x)));
-                        sts2(pf + 1, __fmul2_rn(z1, make_float2(f.y, f.y)));
-                        sts2(pc, z0);
-                        sts2(pc + 1, z1);
-                        if (kk + 1 < NKR) {
-                            z0 = rotate1(z0, w0);
-                            z1 = rotate1(z1, w1);
+                        for (int kk = 0; kk < NKR; ++kk) {
+                            float2* pf = gk + (2 * kk) * (Q * GS);      // (C_k f, S_k f)
+                            float2* pc = gk + (2 * kk + 1) * (Q * GS);  // (C_k, S_k)
+                            // both pixels' pairs in one STS.128 (gp is 16-byte aligned: GS, xl even)
+                            sts4(pf, __fmul2_rn(z0, make_float2(f.x, f.x)), __fmul2_rn(z1, make_float2(f.y, f.y)));
+                            sts4(pc, z0, z1);
+                            if (kk + 1 < NKR) {
+                                z0 = rotate1(z0, w0);
+                                z1 = rotate1(z1, w1);
+                            }
                         }
                     }
                 }
             }
-        }
+        };
+        if (p.border == 2) body(std::true_type{});
+        else body(std::false_type{});
     };
 
     // ---- COMB: combine of step s of segment sg from column buffer cb -----------------
