@@ -196,10 +196,18 @@ def main():
     from paper_1811_02168_b200 import _lib, shard
 
     lib = _lib.load()
+    # FBF_BENCH_FUNCTIONAL=1 (dev): functional check of the multi-rank code paths on a
+    # box with fewer GPUs than ranks (gloo, ranks share devices; numbers meaningless)
+    functional = os.environ.get("FBF_BENCH_FUNCTIONAL") == "1"
+    if functional:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     fb_check = lib.fbf_set_device(local)
     if fb_check != 0:
         raise RuntimeError(_lib.last_error())
@@ -210,7 +218,7 @@ def main():
             dist.barrier()
 
     def max_ranks(*vals):
-        t = torch.tensor(list(vals), dtype=torch.float64, device=dev)
+        t = torch.tensor(list(vals), dtype=torch.float64, device="cpu" if functional else dev)
         if world > 1:
             import torch.distributed as dist
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
