@@ -309,3 +309,27 @@ def test_device_api_on_torch_stream(gpu):
     fb.fast_bilateral_device(d_in, k, a, d_out, d_fallbacks=d_fb, stream=s)
     s.synchronize()
     assert np.array_equal(d_out.cpu().numpy(), host) and int(d_fb.item()) == 0
+
+
+def test_random_shapes_against_oracle(gpu, oracle):
+    # seeded stress: random sizes (incl. widths that are not multiples of the 32-column
+    # strip, heights below the radius), radii 1..30 (pair / split / half modes, Q 8 / 16,
+    # 1..3 coefficient chunks), every border, against the C restatement of the reference
+    fb = gpu
+    rs = np.random.default_rng(20261020)
+    worst = 0.0
+    for case in range(40):
+        w, h = int(rs.integers(1, 150)), int(rs.integers(1, 120))
+        theta = float(rs.choice([0.4, 1.0, 2.5, 3.0, 5.0, 6.7, 10.0]))
+        sigma = float(rs.choice([10.0, 20.0, 35.0, 50.0, 90.0]))
+        eps = float(rs.choice([0.2, 0.1, 0.03]))
+        border = BORDERS[case % 3]
+        img = np.asarray(oracle.random_image(w, h, 500 + case), np.float32)
+        a = fb.select_parameters(sigma, eps=eps)
+        out, fbk = gpu_filter(fb, img, theta, a, border)
+        ref, rfb = oracle_filter(oracle, img, theta, a, border)
+        err = float(np.abs(out - ref).max())
+        worst = max(worst, err)
+        assert fbk == rfb, (case, w, h, theta, sigma, eps, border)
+        assert err <= TOL, (case, w, h, theta, sigma, eps, border, err)
+    assert worst <= TIGHT
