@@ -301,6 +301,15 @@ Plan make_plan(int K, int r) {
             const int mp = qe->max_pairs[pf.ngb][pf.ncb];
             if (mp < 2) continue;
             auto chunks = split_chunks(K, mp);
+            // half mode with 6-7 pairs runs 27-30 warps at 72 / 64 registers: from
+            // r = 22 on the column-half warps' r partial sums spill heavily (measured,
+            // 2048^2, split vs half: K = 4 (7 pairs) r 24 / 27 / 30: 0.59 / 0.56 / 0.56 vs
+            // 0.54 / 0.48 / 0.42; K = 6 r 24 / 30: 0.54 / 0.47 vs 0.50 / 0.40; K = 9 r 30:
+            // 0.45 vs 0.38; at 5 pairs half stays ahead: K = 5 r 27 / 30 0.49 / 0.50 vs
+            // split 0.44 / 0.47; r 18 / 21, K = 4: half 0.47 / 0.51 vs split 0.44 / 0.50)
+            if (fmode < 0 && pf.mode == H && r >= 22 &&
+                std::any_of(chunks.begin(), chunks.end(), [](const Chunk& c) { return c.n_pairs >= 6; }))
+                continue;
             double bal = 1.0;
             for (const Chunk& c : chunks) bal = std::min(bal, subpartition_balance((pf.mode == S ? 2 : 1) * c.n_pairs));
             // rank: 2 pair mode balanced >= 0.85, 1 half mode, 0 the rest (split, unbalanced pair)
