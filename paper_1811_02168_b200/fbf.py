@@ -411,7 +411,7 @@ def fast_bilateral(img, kernel: SpatialKernel, approx: FourierApproximation,
 
 def fast_bilateral_u8(img, kernel: SpatialKernel, approx: FourierApproximation,
                       border=BorderPolicy.symmetric, diag: FilterDiagnostics | None = None,
-                      out_dtype=np.uint8) -> np.ndarray:
+                      out_dtype=np.uint8, out: np.ndarray | None = None) -> np.ndarray:
     """fast_bilateral on an 8-bit image (a PGM payload): 1 byte per pixel crosses
     PCIe. out_dtype uint8: clamped to [0,255] and rounded half away from zero
     on the device (the CLI's write_clamped + write_pgm); float32: the float result."""
@@ -419,7 +419,10 @@ def fast_bilateral_u8(img, kernel: SpatialKernel, approx: FourierApproximation,
     if a.ndim != 2:
         raise InvalidArgument("GrayImage: expected a 2-D (height, width) array")
     c = _approx_args(approx)
-    out = np.empty(a.shape, dtype=np.dtype(out_dtype))
+    if out is None:
+        out = np.empty(a.shape, dtype=np.dtype(out_dtype))  # pass a pinned `out` for full PCIe rate
+    elif out.shape != a.shape or not out.flags.c_contiguous:
+        raise InvalidArgument("fast_bilateral_u8: out must be C-contiguous with the image shape")
     if out.dtype not in (np.uint8, np.float32):
         raise InvalidArgument("fast_bilateral_u8: out_dtype must be uint8 or float32")
     fb = ctypes.c_longlong(0)
