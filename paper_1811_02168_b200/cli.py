@@ -144,7 +144,11 @@ def run_filter(args, g) -> int:
               f"kernel_error={fbf.kernel_error(samples, approx):.6g}", file=sys.stderr)
         t1 = time.perf_counter()
         if img.dtype == np.uint8:
-            out = fbf.fast_bilateral_u8(img, spatial, approx, border, diag)  # clamped + rounded on the device
+            # bytes through pinned staging buffers; clamped + rounded on the device
+            h_in = fbf.pinned_empty(img.shape, np.uint8)
+            h_in[:] = img
+            out = fbf.fast_bilateral_u8(h_in, spatial, approx, border, diag,
+                                        out=fbf.pinned_empty(img.shape, np.uint8))
         else:
             out = np.clip(fbf.fast_bilateral(img, spatial, approx, border, diag), 0.0, 255.0)
         print(f"timing: fit {fit_ms} ms, filter (gpu, host buffers) {_ms(t1)} ms", file=sys.stderr)
