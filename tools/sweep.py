@@ -8,10 +8,10 @@ img = fb.voronoi_image(2048, 2048, 256, 10.0, 42)
 d = torch.from_numpy(img).cuda(); o = torch.empty_like(d)
 n_sm = torch.cuda.get_device_properties(0).multi_processor_count
 peak = n_sm * 128 * 2 * 1965e6
-for r in (3, 6, 9, 12, 15, 18, 24, 30):
+for r in [int(v) for v in os.environ.get("FBF_SWEEP_R", "3 6 9 12 15 18 24 30").split()]:
     theta = r / 3.0
     k = fb.build_spatial_kernel(theta)
-    for K in (2, 3, 4, 5, 7, 9):
+    for K in [int(v) for v in os.environ.get("FBF_SWEEP_K", "2 3 4 5 7 9").split()]:
         a = fb.select_parameters(50.0, K=K, T=200)
         for _ in range(3): fb.fast_bilateral_device(d, k, a, o)
         torch.cuda.synchronize()
