@@ -281,3 +281,18 @@ def test_gpu_brute_large_range_lattice(gpu, ref_lib):
     ref, ref_fb = ref_lib.brute_bilateral(img.astype(np.float64), 2.0, rng, R=R)
     out = fb.brute_bilateral(img, fb.build_spatial_kernel(2.0), fb.RangeKernelSamples(R, rng))
     assert np.array_equal(out, ref)
+
+
+def test_north_star_convenience_call(gpu):
+    # fbf_filter(img, H, W, theta, sigma, eps_or_K, out): eps < 1 -> Algorithm 1, integer
+    # >= 1 -> fixed K with the T scan; Gaussian kernel, R = 255, symmetric border; the
+    # parameters come from the GPU scan and must equal the host selection's
+    fb = gpu
+    img = fb.voronoi_image(131, 77, 12, 10.0, 99)
+    k3 = fb.build_spatial_kernel(3.0)
+    got = fb.fbf_filter(img, 3.0, 30.0, 0.1)
+    want = fb.fast_bilateral(img, k3, fb.select_parameters(30.0, eps=0.1))
+    assert np.array_equal(got, want)
+    got = fb.fbf_filter(img, 3.0, 50.0, 4)
+    want = fb.fast_bilateral(img, k3, fb.select_parameters(50.0, K=4))
+    assert np.array_equal(got, want)
