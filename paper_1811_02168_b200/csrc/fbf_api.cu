@@ -275,7 +275,10 @@ double subpartition_balance(int warps) { return warps / (4.0 * ((warps + 3) / 4)
 // pairs; c4: 0.60 vs 0.51 split), else split mode (c3: 9 pairs, 18 warps 9/10);
 // then the preference list (Q, buffers). FBF_Q, FBF_MODE, FBF_NGB, FBF_NCB
 // override (tuning).
-Plan make_plan(int K, int r) {
+// short_work: fewer than 64 output rows per CTA (small images, c0 512x512: 55): the
+// launch is latency-bound and Q = 16 pair mode wins even with more chunks (c0:
+// 24.7 us in two pair-mode launches vs 26.8 us in one split-mode launch)
+Plan make_plan(int K, int r, bool short_work = false) {
     const auto& ent = fbf_dev::radius_entry(r);
     static const int fq = env_int("FBF_Q"), fngb = env_int("FBF_NGB"), fncb = env_int("FBF_NCB");
     static const int fmode = std::getenv("FBF_MODE") ? env_int("FBF_MODE") : -1;
@@ -315,8 +318,12 @@ Plan make_plan(int K, int r) {
             // rank: 2 pair mode balanced >= 0.85, 1 half mode, 0 the rest (split, unbalanced pair)
             const double rank = pf.mode == P && bal >= 0.85 ? 2 : pf.mode == H ? 1 : 0;
             bal = rank + bal / 2;  // rank first, then balance
-            const bool better = best_bal < 0 || chunks.size() < best.chunks.size() ||
-                                (chunks.size() == best.chunks.size() && bal > best_bal + 1e-9);
+            bool better = best_bal < 0 || chunks.size() < best.chunks.size() ||
+                          (chunks.size() == best.chunks.size() && bal > best_bal + 1e-9);
+            if (short_work && fmode < 0 && best.ent) {
+                const bool cand16 = pf.mode == P && pf.q == 16, best16 = best.mode == P && best.q == 16;
+                if (cand16 != best16) better = cand16;
+            }
             if (better) {
                 best = Plan{std::move(chunks), pf.q, pf.mode, pf.ngb, pf.ncb, qe};
                 best_bal = bal;
@@ -394,7 +401,8 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
             float2* scratch, unsigned long long* d_fallbacks, cudaStream_t stream,
             unsigned int* d_bad = nullptr) {
     const int r = (int)std::ceil(3.0 * theta);
-    const Plan plan = make_plan(a.K, r);
+    const long long units = (long long)job.n_frames * ((job.width + kTW - 1) / kTW) * job.out_rows;
+    const Plan plan = make_plan(a.K, r, units < 64LL * ctx.num_sms);
     if (!plan.ent) return fail(FBF_ECAPACITY, "no kernel variant fits the shared memory for this radius");
     if (plan.chunks.size() > 1 && !scratch) return fail(FBF_EINVAL, "internal: scratch required");
 
@@ -464,7 +472,9 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
 
 size_t scratch_bytes(const Approx& a, double theta, size_t pixels) {
     const int r = (int)std::ceil(3.0 * theta);
-    return make_plan(a.K, r).chunks.size() > 1 ? pixels * sizeof(float2) : 0;
+    // either plan (short_work or not) may run, so size for both
+    const bool chunked = make_plan(a.K, r).chunks.size() > 1 || make_plan(a.K, r, true).chunks.size() > 1;
+    return chunked ? pixels * sizeof(float2) : 0;
 }
 
 size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
