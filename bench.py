@@ -11,7 +11,8 @@ shard one-per-GPU, no collective) -> weak scaling; value = all ranks' pixels /
 max-over-ranks time.
 
 Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA events on
-the launching stream, with a 256 MiB L2 flush (memset) between steps outside
+the launching stream; consecutive steps rotate over input buffers spanning >= 2x
+the L2 (FBF_L2=flush: a 256 MiB memset flush between steps instead), outside
 the events; barrier + synchronize on both sides; max over ranks.
   value      : device-resident megapixels/s (input already in HBM)
   e2e        : the same metric through the public host-buffer API from pinned
@@ -259,22 +260,36 @@ def main():
         d_out = torch.empty_like(d_in)
         work = "one image per rank"
     d_fb = torch.zeros(1, dtype=torch.int64, device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     fb.validate_device(d_in)
+    # L2 (126 MB): consecutive timed steps read different input buffers (and write
+    # different outputs) that together span >= 2x the L2, so no step finds its input
+    # L2-resident -- no flush kernel, no dirty flush lines to write back.
+    # FBF_L2=flush: a 256 MiB memset between steps instead.
+    l2_bytes = 126 << 20
+    flush_mode = os.environ.get("FBF_L2") == "flush"
+    n_rot = 1 if flush_mode else min(256, max(1, -(-2 * l2_bytes // (d_in.numel() * 4))))
+    d_ins = [d_in] + [d_in.clone() for _ in range(n_rot - 1)]
+    d_outs = [d_out] + [torch.empty_like(d_out) for _ in range(n_rot - 1)]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush_mode else None
 
-    def step():
+    def step_noflush(i=0):
+        di, do = d_ins[i % n_rot], d_outs[i % n_rot]
         if mode == "frames":
-            fb.fast_bilateral_batch_device(d_in, kernel, approx, d_out, d_fallbacks=d_fb, stream=stream)
+            fb.fast_bilateral_batch_device(di, kernel, approx, do, d_fallbacks=d_fb, stream=stream)
         elif mode == "bands":
-            fb.fast_bilateral_band_device(d_in, band.src_row0, H, band.out_row0, band.out_rows, kernel, approx,
-                                          d_out, d_fallbacks=d_fb, stream=stream)
+            fb.fast_bilateral_band_device(di, band.src_row0, H, band.out_row0, band.out_rows, kernel, approx,
+                                          do, d_fallbacks=d_fb, stream=stream)
         else:
-            fb.fast_bilateral_device(d_in, kernel, approx, d_out, d_fallbacks=d_fb, stream=stream)
+            fb.fast_bilateral_device(di, kernel, approx, do, d_fallbacks=d_fb, stream=stream)
+
+    def step(i=0):
+        if flush is not None:
+            flush.zero_()
+        step_noflush(i)
 
     with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            flush.zero_()
-            step()
+        for w in range(args.warmup):
+            step(w)
     torch.cuda.synchronize(dev)
     barrier()
     torch.cuda.synchronize(dev)
@@ -282,10 +297,14 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clocks:
         with torch.cuda.stream(stream):
+            # gate: the stream idles ~50 us per step in a sleep kernel while the host
+            # enqueues all timed steps, so no host launch latency lands between events
+            torch.cuda._sleep(int(2e6 + 1e5 * args.steps))
             for s in range(args.steps):
-                flush.zero_()
+                if flush is not None:
+                    flush.zero_()
                 ev[s][0].record(stream)
-                step()
+                step_noflush(args.warmup + s)
                 ev[s][1].record(stream)
         torch.cuda.synchronize(dev)
     launches = lib.fbf_kernel_launches() - launches0
@@ -428,7 +447,9 @@ def main():
                                    + f" image{' per GPU' if mode == 'single' else ''}, theta={cfg.theta} "
                                      f"(r={cfg.radius}), sigma={cfg.sigma}, K={approx.terms}, T={approx.half_period}, "
                                      f"{4 * approx.terms - 2} channels, symmetric border; rank 0: {work}",
-                       "l2": "256 MiB memset flush between timed steps (outside the events)",
+                       "l2": ("256 MiB memset flush between timed steps (outside the events)" if flush_mode else
+                              f"inputs larger than L2: consecutive steps rotate over {n_rot} input/output buffer "
+                              f"pairs ({n_rot} x {d_in.numel() * 4 / 2**20:.1f} MiB in >= 2x the 126 MB L2), no flush"),
                        "parallelism": shards[mode]},
             "gpu_launches": int(launches),
             "e2e": e2e,
