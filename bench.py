@@ -3,15 +3,17 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl ours|reference]
 
-A "step" is one pass of the filtering hot path over one image of the
-configuration (default c1: 2048x2048 Voronoi image, theta=5, sigma=50, fixed
-K=4, T=203 from the host optimiser). Multi-GPU (torchrun, one process per GPU):
-every rank filters its own independent image of that configuration (frames
-shard one-per-GPU, no collective) -> weak scaling; value = all ranks' pixels /
-max-over-ranks time.
+A "step" is one pass of the filtering hot path over the configuration's work
+(default c4, the headline: one 16384x16384 field image, theta=10, sigma=80,
+eps=0.05 -> K=3, T=239 from the host optimiser; the largest BASELINE config that
+fits one B200). Multi-GPU (torchrun, one process per GPU): c4 splits into row
+bands with replicated ceil(3 theta)-row halos, one per rank, and c3's 64 frames
+into contiguous blocks (strong scaling); c0-c2 filter one image per rank (weak
+scaling). No collective on the data path; value = the job's pixels / the
+max-over-ranks median step time.
 
 Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA events on
-the launching stream; consecutive steps rotate over input buffers spanning >= 2x
+the launching stream (value uses the median step); consecutive steps rotate over input buffers spanning >= 2x
 the L2 (FBF_L2=flush: a 256 MiB memset flush between steps instead), outside
 the events; barrier + synchronize on both sides; max over ranks.
   value      : device-resident megapixels/s (input already in HBM)
@@ -23,8 +25,10 @@ the events; barrier + synchronize on both sides; max over ranks.
   roofline   : algorithmic FP32 FLOPs of the fused kernel ((4K-2)*2*(2r+1)*2
                per pixel) / mean launch time, vs the FP32-FMA peak
   cpu_baseline: the reference's own fast_bilateral (oracle/_ref, compiled
-               verbatim, all host threads) on the same image, rank 0, N=1.
---impl reference times that CPU reference as the run itself.
+               verbatim, all host threads) on a bounded sample of the same
+               image (c4: its first 1024 rows), rank 0, N=1.
+--impl reference times that CPU reference as the run itself (same sample; the
+process maps only oracle/ libraries, never libfbf.so).
 """
 from __future__ import annotations
 
@@ -49,7 +53,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="c1")
+    ap.add_argument("--config", default="c4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -124,7 +128,7 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def cpu_reference_run(img, cfg, approx, seconds: float, min_reps: int = 1):
+def cpu_reference_run(img, theta, K, T, coeffs, seconds: float, min_reps: int = 1):
     """Time the reference's fast_bilateral (or the C port) on the host cores."""
     import numpy as np
     from oracle import fbf_oracle
@@ -132,11 +136,10 @@ def cpu_reference_run(img, cfg, approx, seconds: float, min_reps: int = 1):
     img64 = np.ascontiguousarray(img, dtype=np.float64)
     if fbf_oracle.RefLibrary.available():
         lib, kind = fbf_oracle.RefLibrary(), "reference"
-        run = lambda: lib.fast_bilateral(img64, cfg.theta, approx.terms, approx.half_period, approx.coefficients,
-                                         threads=threads)
+        run = lambda: lib.fast_bilateral(img64, theta, K, T, coeffs, threads=threads)
     else:
         lib, kind, threads = fbf_oracle.Oracle(), "port", 1
-        run = lambda: lib.fast_bilateral(img64, cfg.theta, approx.terms, approx.half_period, approx.coefficients)
+        run = lambda: lib.fast_bilateral(img64, theta, K, T, coeffs)
     times = []
     t_end = time.perf_counter() + seconds
     while len(times) < min_reps or time.perf_counter() < t_end:
@@ -149,7 +152,7 @@ def cpu_reference_run(img, cfg, approx, seconds: float, min_reps: int = 1):
 def cpu_sample(cfg, img):
     """The bounded CPU-reference sample of a config: the image (c0-c2), one frame
     (c3), or the first 1024 rows of the 16384x16384 image (c4: the full image
-    takes ~100 s on 8 cores)."""
+    takes ~40 s on 16 cores and ~24 GiB in the reference's FP64 buffers)."""
     if cfg.sharding == "bands" and img.shape[0] > 1024:
         return img[:1024], f"rows [0, 1024) of the {cfg.width}x{cfg.height} image"
     if cfg.sharding == "frames":
@@ -158,26 +161,37 @@ def cpu_sample(cfg, img):
 
 
 def run_reference_impl(args, cfg):
+    """--impl reference: the reference's own fast_bilateral (oracle/_ref, compiled
+    from the reference sources, FP64, all host threads) on a bounded sample of the
+    workload. Inputs come from oracle/build/libfbf_inputs.so (the same generator
+    source, same bits) and (K, T, c) from the oracle's optimiser restatement, so
+    this process never maps libfbf.so (checked below)."""
     rank, world, local = dist_env()
     if rank != 0:
         return
+    from oracle import fbf_oracle
     from paper_1811_02168_b200 import configs
-    img, sample = cpu_sample(cfg, configs.make_frame(cfg, 0))
-    approx = configs.select(cfg)
-    _, _, wt = cpu_reference_run(img, cfg, approx, 0.0, min_reps=max(0, args.warmup))
-    kind, threads, times = cpu_reference_run(img, cfg, approx, 0.0, min_reps=args.steps)
-    total = sum(times)
-    mp = img.size * len(times) / total / 1e6
+    img, sample = cpu_sample(cfg, fbf_oracle.Inputs().make_frame(cfg, 0))
+    rep = fbf_oracle.select_for_config(cfg)
+    assert (rep.K, rep.T) == cfg.expect_KT, (rep.K, rep.T)
+    cpu_reference_run(img, cfg.theta, rep.K, rep.T, rep.coefficients, 0.0, min_reps=max(0, args.warmup))
+    kind, threads, times = cpu_reference_run(img, cfg.theta, rep.K, rep.T, rep.coefficients, 0.0,
+                                             min_reps=args.steps)
+    med = statistics.median(times)
+    mp = img.size / med / 1e6
+    with open("/proc/self/maps") as f:
+        maps = f.read()
+    assert "libfbf.so" not in maps, "reference arm must not map libfbf.so"
     line = {
         "metric": "megapixels_per_sec", "value": round(mp, 4), "unit": "MP/s", "impl": "reference",
-        "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup, "ms_per_step": round(1e3 * med, 3),
         "higher_is_better": True, "scaling": "weak" if cfg.sharding == "single" else "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {cfg.width}x{cfg.height} {cfg.generator} image, theta={cfg.theta}, "
-                               f"sigma={cfg.sigma}, K={approx.terms}, T={approx.half_period}, symmetric border"},
+        "config": {"workload": configs.workload(cfg, rep.K, rep.T)},
         "cpu_baseline": {"value": round(mp, 4), "unit": "MP/s", "cores": threads, "kind": kind,
-                         "sample": f"{sample} per step, fp64 fast_bilateral"},
+                         "sample": f"{sample} per step (median of {len(times)}), fp64 fast_bilateral"},
         "e2e": {"value": round(mp, 4), "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "native_libs": "oracle/_ref/libfbf_ref.so + oracle/build/libfbf_inputs.so; libfbf.so not mapped",
     }
     print(json.dumps(line), flush=True)
 
@@ -309,11 +323,13 @@ def main():
         torch.cuda.synchronize(dev)
     launches = lib.fbf_kernel_launches() - launches0
     barrier()
-    total_ms = sum(a.elapsed_time(b) for a, b in ev)
-    total_ms_max, = max_ranks(total_ms)
-    value = total_px * args.steps / (total_ms_max * 1e-3) / 1e6
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    # the median of the timed steps; max over ranks
+    med_ms, total_ms_max = max_ranks(statistics.median(step_ms), total_ms)
+    value = total_px / (med_ms * 1e-3) / 1e6
     if mode == "single":
-        value = world * local_px * args.steps / (total_ms_max * 1e-3) / 1e6
+        value = world * local_px / (med_ms * 1e-3) / 1e6
 
     # ---- e2e through the host-buffer public API (pinned H2D + D2H inside) ----
     diag = fb.FilterDiagnostics()
@@ -438,15 +454,14 @@ def main():
                   "bands": f"row bands with replicated {cfg.radius}-row halos over {world} GPU(s), no collective"}
         line = {
             "metric": "megapixels_per_sec", "value": round(value, 2), "unit": "MP/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms_max / args.steps, 5),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(med_ms, 5),
+            "ms_per_step_mean": round(total_ms_max / args.steps, 5),
             "higher_is_better": True, "scaling": "weak" if mode == "single" else "strong", "vs_baseline": None,
             "dtype": "f32",
             "data": f"synthetic ({cfg.generator}, {cfg.sites} sites, noise {cfg.noise}, seed {cfg.frame_seed(0)}"
                     + ("+rank)" if mode == "single" else "+frame)" if mode == "frames" else ")"),
-            "config": {"workload": f"{cfg.name}: {W}x{H}" + (f" x{cfg.frames} frames" if mode == "frames" else "")
-                                   + f" image{' per GPU' if mode == 'single' else ''}, theta={cfg.theta} "
-                                     f"(r={cfg.radius}), sigma={cfg.sigma}, K={approx.terms}, T={approx.half_period}, "
-                                     f"{4 * approx.terms - 2} channels, symmetric border; rank 0: {work}",
+            "config": {"workload": configs.workload(cfg, approx.terms, approx.half_period),
+                       "rank0_work": work,
                        "l2": ("256 MiB memset flush between timed steps (outside the events)" if flush_mode else
                               f"inputs larger than L2: consecutive steps rotate over {n_rot} input/output buffer "
                               f"pairs ({n_rot} x {d_in.numel() * 4 / 2**20:.1f} MiB in >= 2x the 126 MB L2), no flush"),
@@ -463,10 +478,11 @@ def main():
         }
         if world == 1 and not args.no_cpu_baseline:
             sample_img, sample = cpu_sample(cfg, img0)
-            kind, threads, times = cpu_reference_run(sample_img, cfg, approx, args.cpu_seconds)
-            mp = sample_img.size * len(times) / sum(times) / 1e6
+            kind, threads, times = cpu_reference_run(sample_img, cfg.theta, approx.terms, approx.half_period,
+                                                     approx.coefficients, args.cpu_seconds)
+            mp = sample_img.size / statistics.median(times) / 1e6
             line["cpu_baseline"] = {"value": round(mp, 4), "unit": "MP/s", "cores": threads, "kind": kind,
-                                    "sample": f"{len(times)} x {sample}, fp64 fast_bilateral"}
+                                    "sample": f"median of {len(times)} x {sample}, fp64 fast_bilateral"}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -25,6 +25,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "build", "libfbf_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libfbf_ref.so")
+INPUTS_SO = os.path.join(HERE, "build", "libfbf_inputs.so")
 
 BORDERS = {"symmetric": 0, "replicate": 1, "zero": 2}
 KINDS = {"gaussian": 0, "exponential": 1, "cauchy": 2}
@@ -222,6 +223,46 @@ class RefLibrary:
         out = np.zeros((h, w))
         self.lib.fbfref_scene_image(w, h, seed, _ptr(out))
         return out
+
+
+class Inputs:
+    """The BASELINE.json input generators (paper_1811_02168_b200/csrc/fbf_synth.cpp
+    compiled on their own into oracle/build/libfbf_inputs.so): bench.py's
+    reference arm builds the same images as the GPU arm without mapping libfbf.so."""
+
+    def __init__(self, path: str = INPUTS_SO):
+        if not os.path.exists(path):
+            build_oracle(with_ref=False)
+        self.lib = ctypes.CDLL(path)
+        fp = ctypes.POINTER(ctypes.c_float)
+        args = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_ulonglong, ctypes.c_int, fp]
+        self.lib.fbf_voronoi_image_f32.argtypes = args
+        self.lib.fbf_field_image_f32.argtypes = args
+        self.lib.fbf_voronoi_image_f32.restype = self.lib.fbf_field_image_f32.restype = None
+
+    def image(self, generator: str, width: int, height: int, sites: int, noise: float, seed: int,
+              threads: int = 0) -> np.ndarray:
+        out = np.empty((height, width), dtype=np.float32)
+        fn = self.lib.fbf_voronoi_image_f32 if generator == "voronoi" else self.lib.fbf_field_image_f32
+        fn(width, height, sites, noise, seed, threads or os.cpu_count() or 1,
+           out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
+        return out
+
+    def make_frame(self, cfg, f: int = 0, threads: int = 0) -> np.ndarray:
+        """configs.make_frame without libfbf.so (same source, same bits)."""
+        return self.image(cfg.generator, cfg.width, cfg.height, cfg.sites, cfg.noise, cfg.frame_seed(f), threads)
+
+
+def select_for_config(cfg, R: int = 255) -> "Report":
+    """(K, T, c) of a BASELINE config by the optimiser restatement below, like the
+    CLI's select_parameters (tools/fourierbf.cpp:185-234): eps -> Algorithm 1,
+    fixed K -> best T over 1..10R then the fixed-period fit."""
+    b = Oracle().range_samples("gaussian", cfg.sigma, R)
+    if cfg.K is not None:
+        T, e = min_error_over_period(cfg.K, b, 10 * R)
+        c, _ = fit_coefficients(design_matrix(cfg.K, T, R), b)
+        return Report(cfg.K, T, c, e)
+    return optimize_parameters(b, cfg.eps)
 
 
 # ---------------------------------------------------------------------------

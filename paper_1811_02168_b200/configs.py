@@ -60,6 +60,13 @@ CONFIGS = {
 }
 
 
+def workload(cfg: Config, K: int, T: int) -> str:
+    """The bench line's config.workload: identical in both arms of bench.py."""
+    shape = f"{cfg.width}x{cfg.height}" + (f" x{cfg.frames} frames" if cfg.frames > 1 else "")
+    return (f"{cfg.name}: {shape} {cfg.generator} image, theta={cfg.theta} (r={cfg.radius}), sigma={cfg.sigma}, "
+            f"K={K}, T={T}, {4 * K - 2} channels, symmetric border")
+
+
 def make_frame(cfg: Config, f: int = 0, threads: int = 0):
     from . import fbf
     seed = cfg.frame_seed(f)
