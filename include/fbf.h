@@ -137,6 +137,30 @@ int fbf_build_lut(const double* sigmas, int n_sigma, const double* epsilons, int
 int fbf_query_lut(const double* sigma_grid, int n_sigma, const double* logeps_grid, int n_eps, const int* K,
                   const int* T, double sigma, double eps, int* K_out, int* T_out);
 /* ---- L3 filter: filter.cpp (the hot path, sm_100a) ---------------------- */
+/* StageTimings (include/fourierbf/filter.hpp:19-24), filled by accumulation
+ * (+=) like filter.cpp:151-211. The kernel fuses channel generation,
+ * convolutions and the combine, so their device time is reported as
+ * convolution_seconds and auxiliary/combine stay 0; fit_seconds is left to the
+ * caller (the reference's CLI fills it, tools/fourierbf.cpp:249-261). The
+ * host-buffer call adds the busy time of its PCIe copies and its wall time. */
+typedef struct fbf_stage_timings {
+    double fit_seconds;
+    double auxiliary_seconds;
+    double convolution_seconds;  /* fused kernel launches, device time (CUDA events) */
+    double combine_seconds;
+    double h2d_seconds;          /* host -> device copies, device time */
+    double d2h_seconds;          /* device -> host copies, device time */
+    double wall_seconds;         /* the whole call on the host clock */
+} fbf_stage_timings;
+
+/* fast_bilateral (filter.hpp:43-46, filter.cpp:129-213) with the whole
+ * FourierApproximation (approx.hpp:14-22): `frequency` is approx.frequency,
+ * used as given like filter.cpp:139 (nu k f is the phase of term k); 0 means
+ * frequency_of(T). timings (optional) as above. Everything else as
+ * fbf_fast_bilateral_f32. */
+int fbf_fast_bilateral_ex(const float* img, int width, int height, double theta, int K, int T, int R,
+                          double frequency, const double* coeffs, int border, float* out, long long* fallbacks,
+                          fbf_stage_timings* timings);
 /* fast_bilateral (filter.hpp:43-46, filter.cpp:129-213) on HOST buffers:
  * validates intensities, copies img to the device, runs the fused kernel,
  * copies out back. K >= 1 coefficients c_0..c_{K-1}, T >= 1, R >= 1.
@@ -153,6 +177,10 @@ int fbf_fast_bilateral_f32(const float* img, int width, int height, double theta
 int fbf_fast_bilateral_f32_device(const float* d_img, int width, int height, double theta, int K,
                                   int T, int R, const double* coeffs, int border, float* d_out,
                                   unsigned long long* d_fallbacks, int device, void* stream);
+/* Device-resident entry points take the scratch of multi-chunk plans (2K-1
+ * channel pairs beyond one launch) from a stream-ordered pool on `stream`,
+ * so concurrent calls on different streams never share buffers. They restore
+ * the calling thread's current device before returning. */
 /* Batch of n_frames independent frames (frame f at img + f*width*height),
  * sharded across the first n_gpus devices (0 -> all), one host thread each;
  * n_gpus = 1 uses the default device (fbf_set_device). Within a device the
@@ -163,7 +191,9 @@ int fbf_fast_bilateral_batch_f32(const float* img, int n_frames, int width, int 
                                  int border, float* out, long long* fallbacks, int n_gpus);
 /* One large image split into n_gpus row bands, each staged with replicated
  * ceil(3 theta)-row halos (border rows keep the mirror semantics); no
- * collective, outputs are disjoint row slices. Bit-identical to n_gpus = 1. */
+ * collective, outputs are disjoint row slices. Bit-identical to n_gpus = 1.
+ * Each device pipelines its band (H2D / kernel / D2H in sub-bands); n_gpus = 1
+ * uses the default device (fbf_set_device). */
 int fbf_fast_bilateral_bands_f32(const float* img, int width, int height, double theta, int K,
                                  int T, int R, const double* coeffs, int border, float* out,
                                  long long* fallbacks, int n_gpus);

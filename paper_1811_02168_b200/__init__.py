@@ -6,7 +6,7 @@ Python mirror of the reference's fbf:: interface.
 """
 from .fbf import (BorderPolicy, ComparisonResult, ImageDelta, brute_bilateral, brute_bilateral_device,
                   compare_images, compare_images_device, compare_with_bound, kernel_error, prop1_bound,
-                  CudaError, FbfError, FilterDiagnostics, FourierApproximation,
+                  CudaError, FbfError, FilterDiagnostics, FourierApproximation, StageTimings,
                   InvalidArgument, OptimizationReport, OptimizeOptions, PerOrderError, PeriodScanResult,
                   RangeKernelKind, RangeKernelSamples, RangeKernelSpec, SpatialKernel, ToleranceUnreachable,
                   band_source_rows, build_spatial_kernel, fast_bilateral, fast_bilateral_band_device,

@@ -53,6 +53,7 @@ SIGNATURES = {
     "fbf_build_lut": (_i, [_dp, _i, _dp, _i, _i, _i, _i, _i, _ip, _ip]),
     "fbf_query_lut": (_i, [_dp, _i, _dp, _i, _ip, _ip, _d, _d, _ip, _ip]),
     "fbf_fast_bilateral_f32": (_i, [_fp, _i, _i, _d, _i, _i, _i, _dp, _i, _fp, _llp]),
+    "fbf_fast_bilateral_ex": (_i, [_fp, _i, _i, _d, _i, _i, _i, _d, _dp, _i, _fp, _llp, _vp]),
     "fbf_fast_bilateral_f32_device": (_i, [_vp, _i, _i, _d, _i, _i, _i, _dp, _i, _vp, _vp, _i, _vp]),
     "fbf_fast_bilateral_batch_f32_device": (_i, [_vp, _i, _i, _i, _d, _i, _i, _i, _dp, _i, _vp, _vp, _i, _vp]),
     "fbf_fast_bilateral_batch_f32": (_i, [_fp, _i, _i, _i, _d, _i, _i, _i, _dp, _i, _fp, _llp, _i]),

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstring>
 #include <atomic>
+#include <chrono>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -26,6 +27,7 @@
 #include <vector>
 
 #include "../../include/fbf.h"
+#include "fbf_cuda_util.h"
 #include "fbf_internal.h"
 #include "fbf_kernel.cuh"
 
@@ -136,6 +138,8 @@ struct DeviceCtx {
     cudaStream_t stream_in = nullptr;   // host -> device copies
     cudaStream_t stream_out = nullptr;  // device -> host copies
     std::vector<cudaEvent_t> events;    // pipelining pool
+    std::vector<cudaEvent_t> tevents;   // timing events (fbf_stage_timings)
+    cudaMemPool_t pool = nullptr;       // stream-ordered scratch of the device-resident calls
     std::mutex mtx;
     void* arena = nullptr;  // cached device scratch
     size_t arena_bytes = 0;
@@ -151,6 +155,26 @@ struct DeviceCtx {
         FBF_CUDA(cudaStreamCreateWithFlags(&stream_out, cudaStreamNonBlocking), "cudaStreamCreate");
         FBF_CUDA(cudaMalloc(&d_counters, 2 * sizeof(unsigned long long)), "cudaMalloc counters");
         FBF_CUDA(cudaMallocHost(&h_counters, 2 * sizeof(unsigned long long)), "cudaMallocHost");
+        // The device-resident entry points take their multi-chunk (num, den) scratch
+        // from this pool in stream order (cudaMallocFromPoolAsync / cudaFreeAsync on
+        // the caller's stream): calls on different streams never share scratch, and
+        // nothing they enqueue touches the host path's arena. Freed blocks stay cached.
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        FBF_CUDA(cudaMemPoolCreate(&pool, &props), "cudaMemPoolCreate");
+        unsigned long long keep = ~0ull;
+        FBF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "cudaMemPoolSetAttribute");
+        return FBF_OK;
+    }
+    int timing_event(size_t i, cudaEvent_t* ev) {
+        while (tevents.size() <= i) {
+            cudaEvent_t e;
+            FBF_CUDA(cudaEventCreate(&e), "cudaEventCreate");
+            tevents.push_back(e);
+        }
+        *ev = tevents[i];
         return FBF_OK;
     }
     int event(size_t i, cudaEvent_t* ev) {
@@ -205,7 +229,14 @@ int get_ctx(int dev, DeviceCtx** out) {
 
 struct Approx {
     int K = 0, T = 0, R = 0;
+    double nu = 0.0;  // approx.frequency (filter.cpp:139); 0 = frequency_of(T)
     std::vector<double> c;
+    // turns per intensity unit, nu / (2 pi), as the kernel's FP32 parameter
+    float turns() const {
+        const double from_T = 2.0 * 3.14159265358979323846 / (2.0 * T + 1.0);
+        if (nu == 0.0 || nu == from_T) return (float)(1.0 / (2.0 * T + 1.0));
+        return (float)(nu / (2.0 * 3.14159265358979323846));
+    }
 };
 
 int check_args(int width, int height, double theta, int K, int T, int R, const double* coeffs,
@@ -460,7 +491,7 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
         p.first_chunk = ci == 0;
         p.last_chunk = ci + 1 == plan.chunks.size();
         for (int kk = 0; kk < c.n_k; ++kk) p.coeff[kk] = (float)a.c[c.k_lo + kk];
-        p.inv_period = (float)(1.0 / (2.0 * a.T + 1.0));
+        p.inv_period = a.turns();
         p.k_first = std::max(c.k_lo, 1);
         if (plan.mode == fbf_dev::kHalfMode) half_mode_placement(c.n_pairs, p);
         const cudaError_t e = plan.ent->launch[nkr](p, grid, stream);
@@ -480,14 +511,7 @@ size_t scratch_bytes(const Approx& a, double theta, size_t pixels) {
 size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
 void source_window(int height, int out_row0, int out_rows, int r, int border, int* row0, int* rows);
-int extent_of(bool bands, int height, int n_frames) { return bands ? height : n_frames; }
 
-// Host-buffer path for n_frames frames on one device. The work is cut into
-// pieces (row bands of a single large image, or groups of frames) and
-// pipelined over three streams: H2D of piece i+1 and D2H of piece i-1 overlap
-// the kernel of piece i; intensity validation is fused into the kernel. Bands read the full device image, so their
-// halos need no extra copies: a band's kernel waits for the copy of the last
-// chunk its border-mapped window reaches. Results are identical to one launch.
 // Host buffers of a call: float32, or 8-bit (PGM payloads) widened / rounded on the device.
 struct HostIO {
     const void* in;
@@ -497,75 +521,117 @@ struct HostIO {
     size_t out_elem() const { return out_u8 ? 1 : sizeof(float); }
 };
 
-int filter_frames_on_device(int dev, const HostIO& io, int n_frames, int width, int height, double theta,
-                            const Approx& a, int border, long long* fallbacks) {
+// What one host-buffer call on one device covers: n_frames whole frames, or
+// (n_frames == 1) output rows [out_row0, out_row0 + out_rows) of a
+// width x height image whose rows [src_row0, src_row0 + src_rows) are at io.in
+// (a row band plus the halo the border mapping reaches; the whole image for a
+// single-image call). io.out receives the output rows only.
+struct Window {
+    int n_frames = 1;
+    int src_row0 = 0, src_rows = 0;
+    int out_row0 = 0, out_rows = 0;
+};
+
+// Stage busy times of a call (fbf_stage_timings), from timing events.
+struct StageClock {
+    double h2d = 0, kernel = 0, d2h = 0;
+};
+
+// Host-buffer path on one device. The work is cut into pieces (row sub-bands
+// of the window, or groups of frames) and pipelined over three streams: H2D of
+// piece i+1 and D2H of piece i-1 overlap the kernel of piece i; intensity
+// validation is fused into the kernel. A sub-band's kernel reads the whole
+// device-resident window, so halos need no extra copies: it waits for the copy
+// of the last source piece its border-mapped rows reach. Results are identical
+// to one launch over the window. On any failure after the first enqueue the
+// three streams are drained before returning, so no copy into or out of the
+// caller's buffers is still in flight (out is then undefined).
+int filter_on_device(int dev, const HostIO& io, const Window& wd, int width, int height, double theta,
+                     const Approx& a, int border, long long* fallbacks, StageClock* clock) {
     DeviceCtx* ctx = nullptr;
     int rc = get_ctx(dev, &ctx);
     if (rc != FBF_OK) return rc;
     std::lock_guard<std::mutex> lock(ctx->mtx);
+    DeviceGuard dguard;
     FBF_CUDA(cudaSetDevice(dev), "cudaSetDevice");
+    const bool bands = wd.n_frames == 1;
     const size_t fp = (size_t)width * height;
-    const size_t pixels = (size_t)n_frames * fp;
-    const size_t img_bytes = align_up(pixels * sizeof(float));
-    const size_t scr = align_up(scratch_bytes(a, theta, pixels));
-    const size_t u8_bytes = align_up(pixels);
-    const size_t in8 = io.in_u8 ? u8_bytes : 0, out8 = io.out_u8 ? u8_bytes : 0;
-    rc = ctx->reserve(2 * img_bytes + scr + in8 + out8);
+    const size_t in_px = bands ? (size_t)wd.src_rows * width : (size_t)wd.n_frames * fp;
+    const size_t out_px = bands ? (size_t)wd.out_rows * width : (size_t)wd.n_frames * fp;
+    const size_t in_bytes = align_up(in_px * sizeof(float)), out_bytes = align_up(out_px * sizeof(float));
+    const size_t scr = align_up(scratch_bytes(a, theta, out_px));
+    const size_t in8 = io.in_u8 ? align_up(in_px) : 0, out8 = io.out_u8 ? align_up(out_px) : 0;
+    rc = ctx->reserve(in_bytes + out_bytes + scr + in8 + out8);
     if (rc != FBF_OK) return rc;
     float* d_in = (float*)ctx->arena;
-    float* d_out = (float*)((char*)ctx->arena + img_bytes);
-    float2* d_scr = scr ? (float2*)((char*)ctx->arena + 2 * img_bytes) : nullptr;
-    unsigned char* d_in8 = (unsigned char*)ctx->arena + 2 * img_bytes + scr;
+    float* d_out = (float*)((char*)ctx->arena + in_bytes);
+    float2* d_scr = scr ? (float2*)((char*)ctx->arena + in_bytes + out_bytes) : nullptr;
+    unsigned char* d_in8 = (unsigned char*)ctx->arena + in_bytes + out_bytes + scr;
     unsigned char* d_out8 = d_in8 + in8;
     const int cvt_grid = ctx->num_sms * 8;
     cudaStream_t sc = ctx->stream, si = ctx->stream_in, so = ctx->stream_out;
+    struct Drain {  // error paths: nothing of this call may still be running afterwards
+        cudaStream_t s[3];
+        bool armed = true;
+        ~Drain() {
+            if (!armed) return;
+            for (cudaStream_t x : s) cudaStreamSynchronize(x);
+            cudaGetLastError();
+        }
+    } drain{{si, sc, so}};
     unsigned int* d_flag = (unsigned int*)(ctx->d_counters + 1);
     const int r = (int)std::ceil(3.0 * theta);
     FBF_CUDA(cudaMemsetAsync(ctx->d_counters, 0, 2 * sizeof(unsigned long long), si), "memset");
 
-    // piece i covers rows [rows0[i], rows0[i+1]) of a single image, or frames [f0, f1)
-    const bool bands = n_frames == 1;
     // bands: one piece per ~4 MiB crossing PCIe (in + out), at most 8 -- more pieces
     // overlap more transfer with compute but each band kernel pays 2r warm-up rows
     // (c1: float32 8 pieces 0.56 ms vs 4 pieces 0.59; 8-bit 2 pieces 0.37 ms vs 8: 0.46)
-    const long long io_bytes = (long long)pixels * (long long)(io.in_elem() + io.out_elem());
+    const long long io_bytes = (long long)in_px * (long long)io.in_elem() + (long long)out_px * io.out_elem();
     int pieces = bands ? (int)std::min<long long>(8, std::max<long long>(1, io_bytes / (4 << 20)))
-                       : std::min(n_frames, 16);
-    if (bands) pieces = std::max(1, std::min(pieces, height / std::max(64, 4 * r)));
-    static const int forced_pieces = [] {
-        const char* e = std::getenv("FBF_PIECES");  // tuning override
-        return e ? std::atoi(e) : 0;
-    }();
-    if (forced_pieces > 0) pieces = std::max(1, std::min(forced_pieces, extent_of(bands, height, n_frames)));
-    std::vector<int> lo(pieces + 1);
-    const int extent = bands ? height : n_frames;
-    for (int i = 0; i <= pieces; ++i) lo[i] = (int)((long long)extent * i / pieces);
+                       : std::min(wd.n_frames, 16);
+    if (bands) pieces = std::max(1, std::min(pieces, wd.out_rows / std::max(64, 4 * r)));
+    static const int forced_pieces = env_int("FBF_PIECES");  // tuning override
+    if (forced_pieces > 0) pieces = std::max(1, std::min(forced_pieces, bands ? wd.out_rows : wd.n_frames));
+    // piece i: output rows [lo[i], lo[i+1]) (global rows) or frames [lo[i], lo[i+1]);
+    // its input copy covers source rows [sb[i], sb[i+1]) (or the same frames)
+    std::vector<int> lo(pieces + 1), sb(pieces + 1);
+    for (int i = 0; i <= pieces; ++i) {
+        lo[i] = bands ? wd.out_row0 + (int)((long long)wd.out_rows * i / pieces)
+                      : (int)((long long)wd.n_frames * i / pieces);
+        sb[i] = bands ? std::clamp(lo[i], wd.src_row0, wd.src_row0 + wd.src_rows) : lo[i];
+    }
+    if (bands) {
+        sb[0] = wd.src_row0;
+        sb[pieces] = wd.src_row0 + wd.src_rows;
+    }
     const size_t unit = bands ? (size_t)width : fp;  // floats per row / per frame
+    const long long in_base = bands ? wd.src_row0 : 0, out_base = bands ? wd.out_row0 : 0;
     cudaEvent_t ev;
-    // dev: FBF_TRACE=1 prints the stage timeline of this call (timing events)
-    static const bool trace = std::getenv("FBF_TRACE") != nullptr;
-    std::vector<std::pair<const char*, cudaEvent_t>> tl;
-    auto mark = [&](const char* what, cudaStream_t st) {
-        if (!trace) return;
+    // timing events per piece: [h2d0, h2d1, k0, k1, d2h0, d2h1]
+    auto tmark = [&](size_t piece, int which, cudaStream_t st) -> int {
+        if (!clock) return FBF_OK;
         cudaEvent_t e;
-        cudaEventCreateWithFlags(&e, cudaEventDefault);
-        cudaEventRecord(e, st);
-        tl.emplace_back(what, e);
+        int rc2 = ctx->timing_event(6 * piece + which, &e);
+        if (rc2 != FBF_OK) return rc2;
+        FBF_CUDA(cudaEventRecord(e, st), "event");
+        return FBF_OK;
     };
-    mark("start", si);
     for (int i = 0; i < pieces; ++i) {
-        const size_t off = (size_t)lo[i] * unit, n = (size_t)(lo[i + 1] - lo[i]) * unit;
-        if (io.in_u8) {
-            FBF_CUDA(cudaMemcpyAsync(d_in8 + off, (const unsigned char*)io.in + off, n, cudaMemcpyHostToDevice, si),
-                     "H2D");
-            fbf_dev::u8_to_f32_kernel<<<cvt_grid, 256, 0, si>>>(d_in8 + off, d_in + off, n);
-            FBF_CUDA(cudaGetLastError(), "u8 widen launch");
-            g_launches += 1;
-        } else {
-            FBF_CUDA(cudaMemcpyAsync(d_in + off, (const float*)io.in + off, n * sizeof(float), cudaMemcpyHostToDevice,
-                                     si), "H2D");
+        const size_t off = (size_t)(sb[i] - in_base) * unit, n = (size_t)(sb[i + 1] - sb[i]) * unit;
+        if ((rc = tmark(i, 0, si)) != FBF_OK) return rc;
+        if (n > 0) {
+            if (io.in_u8) {
+                FBF_CUDA(cudaMemcpyAsync(d_in8 + off, (const unsigned char*)io.in + off, n, cudaMemcpyHostToDevice,
+                                         si), "H2D");
+                fbf_dev::u8_to_f32_kernel<<<cvt_grid, 256, 0, si>>>(d_in8 + off, d_in + off, n);
+                FBF_CUDA(cudaGetLastError(), "u8 widen launch");
+                g_launches += 1;
+            } else {
+                FBF_CUDA(cudaMemcpyAsync(d_in + off, (const float*)io.in + off, n * sizeof(float),
+                                         cudaMemcpyHostToDevice, si), "H2D");
+            }
         }
-        mark("in", si);
+        if ((rc = tmark(i, 1, si)) != FBF_OK) return rc;
         if ((rc = ctx->event(2 * i, &ev)) != FBF_OK) return rc;
         FBF_CUDA(cudaEventRecord(ev, si), "event");
     }
@@ -574,59 +640,65 @@ int filter_frames_on_device(int dev, const HostIO& io, int n_frames, int width, 
         if (bands) {
             int s0 = 0, sn = 0;
             source_window(height, lo[i], lo[i + 1] - lo[i], r, border, &s0, &sn);
-            while (need + 1 < pieces && lo[need + 1] < s0 + sn) ++need;
+            need = 0;
+            while (need + 1 < pieces && sb[need + 1] < s0 + sn) ++need;
         }
         if ((rc = ctx->event(2 * need, &ev)) != FBF_OK) return rc;
         FBF_CUDA(cudaStreamWaitEvent(sc, ev, 0), "wait");
-        Job job = bands ? Job{d_in, (long long)fp, 0, height, d_out + (size_t)lo[i] * width, (long long)fp,
-                              width, height, 1, lo[i], lo[i + 1] - lo[i]}
+        Job job = bands ? Job{d_in, (long long)fp, wd.src_row0, wd.src_rows, d_out + (size_t)(lo[i] - out_base) * width,
+                              (long long)fp, width, height, 1, lo[i], lo[i + 1] - lo[i]}
                         : Job{d_in + (size_t)lo[i] * fp, (long long)fp, 0, height, d_out + (size_t)lo[i] * fp,
                               (long long)fp, width, height, lo[i + 1] - lo[i], 0, height};
-        float2* sp = d_scr ? d_scr + (size_t)lo[i] * unit : nullptr;
+        const size_t ooff = (size_t)(lo[i] - out_base) * unit, on = (size_t)(lo[i + 1] - lo[i]) * unit;
+        float2* sp = d_scr ? d_scr + ooff : nullptr;
+        if ((rc = tmark(i, 2, sc)) != FBF_OK) return rc;
         // intensity validation runs inside the kernel (every pixel is combined once)
-        mark("k0", sc);
         rc = run_job(*ctx, job, theta, a, border, sp, ctx->d_counters, sc, d_flag);
         if (rc != FBF_OK) return rc;
-        mark("k1", sc);
-        const size_t off = (size_t)lo[i] * unit, n = (size_t)(lo[i + 1] - lo[i]) * unit;
         if (io.out_u8) {
-            fbf_dev::f32_to_u8_kernel<<<cvt_grid, 256, 0, sc>>>(d_out + off, d_out8 + off, n);
+            fbf_dev::f32_to_u8_kernel<<<cvt_grid, 256, 0, sc>>>(d_out + ooff, d_out8 + ooff, on);
             FBF_CUDA(cudaGetLastError(), "u8 round launch");
             g_launches += 1;
         }
+        if ((rc = tmark(i, 3, sc)) != FBF_OK) return rc;
         if ((rc = ctx->event(2 * i + 1, &ev)) != FBF_OK) return rc;
         FBF_CUDA(cudaEventRecord(ev, sc), "event");
         FBF_CUDA(cudaStreamWaitEvent(so, ev, 0), "wait");
+        if ((rc = tmark(i, 4, so)) != FBF_OK) return rc;
         if (io.out_u8)
-            FBF_CUDA(cudaMemcpyAsync((unsigned char*)io.out + off, d_out8 + off, n, cudaMemcpyDeviceToHost, so), "D2H");
-        else
-            FBF_CUDA(cudaMemcpyAsync((float*)io.out + off, d_out + off, n * sizeof(float), cudaMemcpyDeviceToHost, so),
+            FBF_CUDA(cudaMemcpyAsync((unsigned char*)io.out + ooff, d_out8 + ooff, on, cudaMemcpyDeviceToHost, so),
                      "D2H");
-        mark("out", so);
+        else
+            FBF_CUDA(cudaMemcpyAsync((float*)io.out + ooff, d_out + ooff, on * sizeof(float), cudaMemcpyDeviceToHost,
+                                     so), "D2H");
+        if ((rc = tmark(i, 5, so)) != FBF_OK) return rc;
     }
     FBF_CUDA(cudaMemcpyAsync(ctx->h_counters, ctx->d_counters, 2 * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, so), "D2H counters");
     FBF_CUDA(cudaStreamSynchronize(so), "filter");
-    if (trace) {
-        cudaDeviceSynchronize();
-        std::string line = "fbf trace (us):";
-        for (auto& [what, e] : tl) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, tl[0].second, e);
-            line += std::string(" ") + what + "=" + std::to_string((int)(ms * 1000.f));
+    drain.armed = false;
+    if (clock) {
+        for (int i = 0; i < pieces; ++i) {
+            float ms[3] = {0, 0, 0};
+            for (int k = 0; k < 3; ++k)
+                FBF_CUDA(cudaEventElapsedTime(&ms[k], ctx->tevents[6 * i + 2 * k], ctx->tevents[6 * i + 2 * k + 1]),
+                         "timing");
+            clock->h2d += 1e-3 * ms[0];
+            clock->kernel += 1e-3 * ms[1];
+            clock->d2h += 1e-3 * ms[2];
         }
-        for (auto& [what, e] : tl) cudaEventDestroy(e);
-        std::fprintf(stderr, "%s\n", line.c_str());
     }
     if (ctx->h_counters[1]) return fail(FBF_ERANGE, "filter: pixel intensity outside [0, R]");
     if (fallbacks) *fallbacks += (long long)ctx->h_counters[0];
     return FBF_OK;
 }
 
-int make_approx(int K, int T, int R, const double* coeffs, Approx& a) {
+int make_approx(int K, int T, int R, const double* coeffs, Approx& a, double frequency = 0.0) {
     a.K = K;
     a.T = T;
     a.R = R;
+    if (!std::isfinite(frequency)) return fail(FBF_EINVAL, "fast_bilateral: non-finite frequency");
+    a.nu = frequency;
     a.c.assign(coeffs, coeffs + K);
     for (double v : a.c)
         if (!std::isfinite(v)) return fail(FBF_EINVAL, "fast_bilateral: non-finite coefficient");
@@ -674,6 +746,36 @@ void source_window(int height, int out_row0, int out_rows, int r, int border, in
     for (int y = out_row0 + out_rows; y < out_row0 + out_rows + r; ++y) widen(y);
     *row0 = lo;
     *rows = hi - lo;
+}
+
+// Device-resident job on the caller's stream; multi-chunk scratch from the
+// context's stream-ordered pool (allocated and freed on `st`).
+int run_device_job(int device, const Job& job, double theta, const Approx& a, int border,
+                   unsigned long long* d_fallbacks, cudaStream_t st) {
+    DeviceCtx* ctx = nullptr;
+    int rc = get_ctx(device, &ctx);
+    if (rc != FBF_OK) return rc;
+    DeviceGuard dguard;
+    FBF_CUDA(cudaSetDevice(device), "cudaSetDevice");
+    const size_t scr = scratch_bytes(a, theta, (size_t)job.n_frames * job.out_rows * job.width);
+    float2* d_scr = nullptr;
+    if (scr) {
+        const cudaError_t e = cudaMallocFromPoolAsync((void**)&d_scr, scr, ctx->pool, st);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(e == cudaErrorMemoryAllocation ? FBF_ENOMEM : FBF_ECUDA,
+                        std::string("scratch allocation: ") + cudaGetErrorString(e));
+        }
+    }
+    rc = run_job(*ctx, job, theta, a, border, d_scr, d_fallbacks, st);
+    if (d_scr) cudaFreeAsync(d_scr, st);
+    return rc;
+}
+
+int band_of(int height, int G, int g, int* y0, int* y1) {
+    *y0 = (int)((long long)height * g / G);
+    *y1 = (int)((long long)height * (g + 1) / G);
+    return *y1 - *y0;
 }
 
 }  // namespace
@@ -748,6 +850,7 @@ int fbf_validate_f32_device(const float* d_img, size_t n, int R, int device, voi
     int rc = get_ctx(device, &ctx);
     if (rc != FBF_OK) return rc;
     std::lock_guard<std::mutex> lock(ctx->mtx);
+    DeviceGuard dguard;
     FBF_CUDA(cudaSetDevice(device), "cudaSetDevice");
     cudaStream_t st = (cudaStream_t)stream;  // NULL = the legacy default stream
     FBF_CUDA(cudaMemsetAsync(ctx->d_counters + 1, 0, sizeof(unsigned long long), st), "memset");
@@ -761,18 +864,35 @@ int fbf_validate_f32_device(const float* d_img, size_t n, int R, int device, voi
     return FBF_OK;
 }
 
-int fbf_fast_bilateral_f32(const float* img, int width, int height, double theta, int K, int T, int R,
-                           const double* coeffs, int border, float* out, long long* fallbacks) {
+int fbf_fast_bilateral_ex(const float* img, int width, int height, double theta, int K, int T, int R,
+                          double frequency, const double* coeffs, int border, float* out, long long* fallbacks,
+                          fbf_stage_timings* timings) {
+    const auto t0 = std::chrono::steady_clock::now();
     int r = 0;
     int rc = check_args(width, height, theta, K, T, R, coeffs, border, &r);
     if (rc != FBF_OK) return rc;
+    if (!img || !out) return fail(FBF_EINVAL, "fast_bilateral: null image buffer");
     Approx a;
-    rc = make_approx(K, T, R, coeffs, a);
+    rc = make_approx(K, T, R, coeffs, a, frequency);
     if (rc != FBF_OK) return rc;
-    rc = filter_frames_on_device(g_default_device.load(), HostIO{img, out}, 1, width, height, theta, a, border,
-                                 fallbacks);
-    if (rc == FBF_OK) clear_error();
-    return rc;
+    StageClock clock;
+    Window wd{1, 0, height, 0, height};
+    rc = filter_on_device(g_default_device.load(), HostIO{img, out}, wd, width, height, theta, a, border, fallbacks,
+                          timings ? &clock : nullptr);
+    if (rc != FBF_OK) return rc;
+    if (timings) {  // accumulated like StageTimings (filter.cpp:151-211)
+        timings->convolution_seconds += clock.kernel;
+        timings->h2d_seconds += clock.h2d;
+        timings->d2h_seconds += clock.d2h;
+        timings->wall_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    clear_error();
+    return FBF_OK;
+}
+
+int fbf_fast_bilateral_f32(const float* img, int width, int height, double theta, int K, int T, int R,
+                           const double* coeffs, int border, float* out, long long* fallbacks) {
+    return fbf_fast_bilateral_ex(img, width, height, theta, K, T, R, 0.0, coeffs, border, out, fallbacks, nullptr);
 }
 
 int fbf_fast_bilateral_f32_device(const float* d_img, int width, int height, double theta, int K, int T,
@@ -798,21 +918,8 @@ int fbf_fast_bilateral_band_f32_device(const float* d_src, int src_row0, int src
     Approx a;
     rc = make_approx(K, T, R, coeffs, a);
     if (rc != FBF_OK) return rc;
-    DeviceCtx* ctx = nullptr;
-    rc = get_ctx(device, &ctx);
-    if (rc != FBF_OK) return rc;
-    std::lock_guard<std::mutex> lock(ctx->mtx);
-    FBF_CUDA(cudaSetDevice(device), "cudaSetDevice");
-    cudaStream_t st = (cudaStream_t)stream;  // NULL = the legacy default stream
-    const size_t scr = scratch_bytes(a, theta, (size_t)out_rows * width);
-    float2* d_scr = nullptr;
-    if (scr) {
-        rc = ctx->reserve(scr);
-        if (rc != FBF_OK) return rc;
-        d_scr = (float2*)ctx->arena;
-    }
     Job job{d_src, 0, src_row0, src_rows, d_dst, 0, width, height, 1, out_row0, out_rows};
-    rc = run_job(*ctx, job, theta, a, border, d_scr, d_fallbacks, st);
+    rc = run_device_job(device, job, theta, a, border, d_fallbacks, (cudaStream_t)stream);
     if (rc == FBF_OK) clear_error();
     return rc;
 }
@@ -827,23 +934,10 @@ int fbf_fast_bilateral_batch_f32_device(const float* d_img, int n_frames, int wi
     Approx a;
     rc = make_approx(K, T, R, coeffs, a);
     if (rc != FBF_OK) return rc;
-    DeviceCtx* ctx = nullptr;
-    rc = get_ctx(device, &ctx);
-    if (rc != FBF_OK) return rc;
-    std::lock_guard<std::mutex> lock(ctx->mtx);
-    FBF_CUDA(cudaSetDevice(device), "cudaSetDevice");
-    cudaStream_t st = (cudaStream_t)stream;
     const size_t fp = (size_t)width * height;
-    const size_t scr = scratch_bytes(a, theta, (size_t)n_frames * fp);
-    float2* d_scr = nullptr;
-    if (scr) {
-        rc = ctx->reserve(scr);
-        if (rc != FBF_OK) return rc;
-        d_scr = (float2*)ctx->arena;
-    }
     // one launch over all frames: CTAs take contiguous (frame, strip, row) shares
     Job job{d_img, (long long)fp, 0, height, d_out, (long long)fp, width, height, n_frames, 0, height};
-    rc = run_job(*ctx, job, theta, a, border, d_scr, d_fallbacks, st);
+    rc = run_device_job(device, job, theta, a, border, d_fallbacks, (cudaStream_t)stream);
     if (rc == FBF_OK) clear_error();
     return rc;
 }
@@ -876,8 +970,9 @@ int fbf_fast_bilateral_batch_f32(const float* img, int n_frames, int width, int 
         const int f0 = (int)((long long)n_frames * g / G), f1 = (int)((long long)n_frames * (g + 1) / G);
         // one device: the process's default device (fbf_set_device), e.g. its local rank
         const int dev = G == 1 ? g_default_device.load() : g;
-        return filter_frames_on_device(dev, HostIO{img + f0 * fp, out + f0 * fp}, f1 - f0, width, height, theta, a,
-                                       border, &fb[g]);
+        Window wd{f1 - f0, 0, height, 0, height};
+        return filter_on_device(dev, HostIO{img + f0 * fp, out + f0 * fp}, wd, width, height, theta, a, border,
+                                &fb[g], nullptr);
     });
     if (rc != FBF_OK) return rc;
     if (fallbacks)
@@ -900,39 +995,17 @@ int fbf_fast_bilateral_bands_f32(const float* img, int width, int height, double
     if (rc != FBF_OK) return rc;
     G = std::max(1, std::min(G, height));
     std::vector<long long> fb(G, 0);
+    // one host thread per device; each device pipelines its band + halo window
+    // (H2D / kernel / D2H in sub-bands, like the single-image call)
     rc = per_device(G, [&](int g) -> int {
-        const int y0 = (int)((long long)height * g / G), y1 = (int)((long long)height * (g + 1) / G);
+        int y0 = 0, y1 = 0;
+        band_of(height, G, g, &y0, &y1);
         int s0 = 0, sn = 0;
         source_window(height, y0, y1 - y0, r, border, &s0, &sn);
-        DeviceCtx* ctx = nullptr;
-        int rc2 = get_ctx(g, &ctx);
-        if (rc2 != FBF_OK) return rc2;
-        std::lock_guard<std::mutex> lock(ctx->mtx);
-        FBF_CUDA(cudaSetDevice(g), "cudaSetDevice");
-        const size_t in_b = align_up((size_t)sn * width * sizeof(float));
-        const size_t out_b = align_up((size_t)(y1 - y0) * width * sizeof(float));
-        const size_t scr = align_up(scratch_bytes(a, theta, (size_t)(y1 - y0) * width));
-        rc2 = ctx->reserve(in_b + out_b + scr);
-        if (rc2 != FBF_OK) return rc2;
-        float* d_in = (float*)ctx->arena;
-        float* d_out = (float*)((char*)ctx->arena + in_b);
-        float2* d_scr = scr ? (float2*)((char*)ctx->arena + in_b + out_b) : nullptr;
-        cudaStream_t st = ctx->stream;
-        FBF_CUDA(cudaMemsetAsync(ctx->d_counters, 0, 2 * sizeof(unsigned long long), st), "memset");
-        FBF_CUDA(cudaMemcpyAsync(d_in, img + (size_t)s0 * width, (size_t)sn * width * sizeof(float),
-                                 cudaMemcpyHostToDevice, st), "H2D band");
-        Job job{d_in, 0, s0, sn, d_out, 0, width, height, 1, y0, y1 - y0};
-        rc2 = run_job(*ctx, job, theta, a, border, d_scr, ctx->d_counters, st,
-                      (unsigned int*)(ctx->d_counters + 1));  // validation fused into the combine
-        if (rc2 != FBF_OK) return rc2;
-        FBF_CUDA(cudaMemcpyAsync(out + (size_t)y0 * width, d_out, (size_t)(y1 - y0) * width * sizeof(float),
-                                 cudaMemcpyDeviceToHost, st), "D2H band");
-        FBF_CUDA(cudaMemcpyAsync(ctx->h_counters, ctx->d_counters, 2 * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, st), "D2H counters");
-        FBF_CUDA(cudaStreamSynchronize(st), "bands");
-        if (ctx->h_counters[1]) return fail(FBF_ERANGE, "filter: pixel intensity outside [0, R]");
-        fb[g] = (long long)ctx->h_counters[0];
-        return FBF_OK;
+        const int dev = G == 1 ? g_default_device.load() : g;
+        Window wd{1, s0, sn, y0, y1 - y0};
+        return filter_on_device(dev, HostIO{img + (size_t)s0 * width, out + (size_t)y0 * width}, wd, width, height,
+                                theta, a, border, &fb[g], nullptr);
     });
     if (rc != FBF_OK) return rc;
     if (fallbacks)
@@ -953,7 +1026,8 @@ int fbf_fast_bilateral_u8(const unsigned char* img, int width, int height, doubl
     rc = make_approx(K, T, R, coeffs, a);
     if (rc != FBF_OK) return rc;
     HostIO io{img, out_u8 ? (void*)out_u8 : (void*)out_f32, true, out_u8 != nullptr};
-    rc = filter_frames_on_device(g_default_device.load(), io, 1, width, height, theta, a, border, fallbacks);
+    Window wd{1, 0, height, 0, height};
+    rc = filter_on_device(g_default_device.load(), io, wd, width, height, theta, a, border, fallbacks, nullptr);
     if (rc == FBF_OK) clear_error();
     return rc;
 }

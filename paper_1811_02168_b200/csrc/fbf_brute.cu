@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "../../include/fbf.h"
+#include "fbf_cuda_util.h"
 #include "fbf_internal.h"
 
 namespace fbf_dev {
@@ -218,6 +219,7 @@ int fbf_brute_bilateral_f32_device(const float* d_img, int width, int height, do
     void* sv = nullptr;
     std::mutex* mtx = nullptr;
     if ((rc = device_context(device, &sv, &mtx)) != FBF_OK) return rc;
+    DeviceGuard dguard;
     FBF_CU(cudaSetDevice(device), "cudaSetDevice");
     cudaStream_t st = (cudaStream_t)stream;
     DevBuf params;
@@ -243,6 +245,7 @@ int fbf_brute_bilateral_f32(const float* img, int width, int height, double thet
     std::mutex* mtx = nullptr;
     if ((rc = device_context(device, &sv, &mtx)) != FBF_OK) return rc;
     std::lock_guard<std::mutex> lock(*mtx);
+    DeviceGuard dguard;
     FBF_CU(cudaSetDevice(device), "cudaSetDevice");
     cudaStream_t st = (cudaStream_t)sv;
     DevBuf d_img, d_out, d_params, d_fb;
@@ -271,6 +274,7 @@ int fbf_compare_images_device(const double* d_ref, const float* d_cand, size_t n
     void* sv = nullptr;
     std::mutex* mtx = nullptr;
     if ((rc = device_context(device, &sv, &mtx)) != FBF_OK) return rc;
+    DeviceGuard dguard;
     FBF_CU(cudaSetDevice(device), "cudaSetDevice");
     cudaStream_t st = (cudaStream_t)stream;
     DevBuf part;

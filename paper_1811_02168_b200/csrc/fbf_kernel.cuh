@@ -44,6 +44,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <type_traits>
 
 namespace fbf_dev {
@@ -1070,12 +1071,20 @@ template <int R, int Q, int NKR, int M>
 cudaError_t launch_fused(const Params& p, int grid, cudaStream_t stream) {
     using G = Geometry<R, Q, M>;
     const size_t smem = G::smem_bytes(p.n_pairs, p.ngb, p.ncb);
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fbf_fused_kernel<R, Q, NKR, M>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
+    // The dynamic shared-memory opt-in is a property of the function in the
+    // CURRENT device's context: set it once per device (bit d of the mask), safe
+    // against concurrent launches from the per-device host threads (a second
+    // setter only repeats an idempotent call).
+    static std::atomic<unsigned long long> configured{0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(configured.load(std::memory_order_acquire) & bit)) {
+        e = cudaFuncSetAttribute(fbf_fused_kernel<R, Q, NKR, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSmemLimit);
         if (e != cudaSuccess) return e;
-        configured = true;
+        configured.fetch_or(bit, std::memory_order_acq_rel);
     }
     fbf_fused_kernel<R, Q, NKR, M><<<grid, block_threads(p.n_pairs, M), smem, stream>>>(p);
     return cudaGetLastError();

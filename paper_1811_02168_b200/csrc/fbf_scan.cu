@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "../../include/fbf.h"
+#include "fbf_cuda_util.h"
 #include "fbf_internal.h"
 
 namespace fbf_dev {
@@ -283,6 +284,7 @@ int gpu_scan_errors(const double* samples, int R, int K_lo, int nK, int t_max, i
         cleanup();
         return fail(FBF_ECUDA, std::string("gpu period scan: ") + what + ": " + cudaGetErrorString(e));
     };
+    DeviceGuard dguard;
     if ((rc = cu(cudaSetDevice(device), "cudaSetDevice")) != FBF_OK) return rc;
     if ((rc = cu(cudaMalloc(&d_b, sizeof(double) * m), "cudaMalloc")) != FBF_OK) return rc;
     if ((rc = cu(cudaMalloc(&d_e, sizeof(double) * n), "cudaMalloc")) != FBF_OK) return rc;

@@ -373,6 +373,26 @@ class FilterDiagnostics:
     fallback_pixels: int = 0
 
 
+class _StageTimingsC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("fit_seconds", "auxiliary_seconds", "convolution_seconds",
+                                                "combine_seconds", "h2d_seconds", "d2h_seconds", "wall_seconds")]
+
+
+@dataclass
+class StageTimings:
+    """filter.hpp:19-24, accumulated like filter.cpp:151-211. The fused kernel's
+    device time is convolution_seconds (channel generation and the combine run
+    inside it, so auxiliary_seconds and combine_seconds stay 0); h2d / d2h /
+    wall are the host-buffer call's copy busy times and wall time."""
+    fit_seconds: float = 0.0
+    auxiliary_seconds: float = 0.0
+    convolution_seconds: float = 0.0
+    combine_seconds: float = 0.0
+    h2d_seconds: float = 0.0
+    d2h_seconds: float = 0.0
+    wall_seconds: float = 0.0
+
+
 def _as_image(img) -> np.ndarray:
     a = np.asarray(img)
     if a.ndim != 2:
@@ -388,11 +408,13 @@ def _approx_args(approx: FourierApproximation):
 
 def fast_bilateral(img, kernel: SpatialKernel, approx: FourierApproximation,
                    border=BorderPolicy.symmetric, diag: FilterDiagnostics | None = None,
-                   out: np.ndarray | None = None) -> np.ndarray:
+                   out: np.ndarray | None = None, timings: StageTimings | None = None) -> np.ndarray:
     """filter.hpp:43-46 / filter.cpp:129-213 on the GPU (host buffers in, host buffer out).
 
+    approx.frequency is used as given (filter.cpp:139; 0 = frequency_of(T)).
     `out` (optional) is a caller-owned float32 (H, W) C-contiguous array, e.g.
-    a view of pinned memory, written in place.
+    a view of pinned memory, written in place. `timings` (optional) accumulates
+    the stage times (StageTimings).
     """
     a = _as_image(img)
     c = _approx_args(approx)
@@ -401,11 +423,16 @@ def fast_bilateral(img, kernel: SpatialKernel, approx: FourierApproximation,
     elif out.dtype != np.float32 or out.shape != a.shape or not out.flags.c_contiguous:
         raise InvalidArgument("out must be a C-contiguous float32 array of the image shape")
     fb = ctypes.c_longlong(0)
-    _check(_lib.load().fbf_fast_bilateral_f32(_fptr(a), a.shape[1], a.shape[0], kernel.theta, approx.terms,
-                                              approx.half_period, approx.dynamic_range, _dptr(c), _border(border),
-                                              _fptr(out), ctypes.byref(fb)))
+    st = _StageTimingsC() if timings is not None else None
+    _check(_lib.load().fbf_fast_bilateral_ex(_fptr(a), a.shape[1], a.shape[0], kernel.theta, approx.terms,
+                                             approx.half_period, approx.dynamic_range, float(approx.frequency),
+                                             _dptr(c), _border(border), _fptr(out), ctypes.byref(fb),
+                                             ctypes.byref(st) if st is not None else None))
     if diag is not None:
         diag.fallback_pixels += fb.value
+    if timings is not None:
+        for name, _ in _StageTimingsC._fields_:
+            setattr(timings, name, getattr(timings, name) + getattr(st, name))
     return out
 
 
@@ -484,6 +511,30 @@ def band_source_rows(height: int, out_row0: int, out_rows: int, theta: float,
     return r0.value, n.value
 
 
+def _check_device_tensor(t, what: str, shape, device, dtype=None) -> None:
+    """A device buffer handed to the kernel as a raw pointer: contiguous, of the
+    expected dtype (float32 by default) and shape, on the input's device."""
+    import torch
+    dtype = dtype or torch.float32
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise InvalidArgument(f"{what} must be a CUDA tensor")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise InvalidArgument(f"{what} must be a contiguous {dtype} CUDA tensor")
+    if tuple(t.shape) != tuple(shape):
+        raise InvalidArgument(f"{what} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if t.device != device:
+        raise InvalidArgument(f"{what} is on {t.device}, the input on {device}")
+
+
+def _check_fallbacks(d_fallbacks, device) -> None:
+    import torch
+    if d_fallbacks is None:
+        return
+    if (not isinstance(d_fallbacks, torch.Tensor) or not d_fallbacks.is_cuda or d_fallbacks.device != device
+            or d_fallbacks.dtype not in (torch.int64, torch.uint64) or d_fallbacks.numel() < 1):
+        raise InvalidArgument("d_fallbacks must be a 64-bit integer CUDA tensor on the input's device")
+
+
 def fast_bilateral_device(d_img, kernel: SpatialKernel, approx: FourierApproximation, d_out,
                           border=BorderPolicy.symmetric, d_fallbacks=None, stream=None) -> None:
     """Device-resident variant on torch CUDA tensors (float32, contiguous, (H, W)).
@@ -492,8 +543,11 @@ def fast_bilateral_device(d_img, kernel: SpatialKernel, approx: FourierApproxima
     without synchronising. No intensity validation (see validate_device).
     """
     import torch
-    if d_img.dtype != torch.float32 or not d_img.is_cuda or not d_img.is_contiguous():
-        raise InvalidArgument("device image must be a contiguous float32 CUDA tensor")
+    if not isinstance(d_img, torch.Tensor) or d_img.dim() != 2:
+        raise InvalidArgument("device image must be a 2-D (H, W) CUDA tensor")
+    _check_device_tensor(d_img, "device image", d_img.shape, d_img.device)
+    _check_device_tensor(d_out, "d_out", d_img.shape, d_img.device)
+    _check_fallbacks(d_fallbacks, d_img.device)
     H, W = d_img.shape
     c = _approx_args(approx)
     st = stream if stream is not None else torch.cuda.current_stream(d_img.device)
@@ -508,8 +562,11 @@ def fast_bilateral_batch_device(d_frames, kernel: SpatialKernel, approx: Fourier
                                 border=BorderPolicy.symmetric, d_fallbacks=None, stream=None) -> None:
     """Device-resident batch (n_frames, H, W) float32 CUDA tensors, one launch."""
     import torch
-    if d_frames.dtype != torch.float32 or not d_frames.is_cuda or not d_frames.is_contiguous() or d_frames.dim() != 3:
+    if not isinstance(d_frames, torch.Tensor) or d_frames.dim() != 3:
         raise InvalidArgument("device frames must be a contiguous (n, H, W) float32 CUDA tensor")
+    _check_device_tensor(d_frames, "device frames", d_frames.shape, d_frames.device)
+    _check_device_tensor(d_out, "d_out", d_frames.shape, d_frames.device)
+    _check_fallbacks(d_fallbacks, d_frames.device)
     n, H, W = d_frames.shape
     c = _approx_args(approx)
     st = stream if stream is not None else torch.cuda.current_stream(d_frames.device)
@@ -523,9 +580,15 @@ def fast_bilateral_batch_device(d_frames, kernel: SpatialKernel, approx: Fourier
 def fast_bilateral_band_device(d_src, src_row0: int, height: int, out_row0: int, out_rows: int,
                                kernel: SpatialKernel, approx: FourierApproximation, d_dst,
                                border=BorderPolicy.symmetric, d_fallbacks=None, stream=None) -> None:
-    """One rank's band: d_src holds global rows [src_row0, src_row0 + d_src.shape[0])."""
+    """One rank's band: d_src holds global rows [src_row0, src_row0 + d_src.shape[0]);
+    d_dst (out_rows, W) receives output rows [out_row0, out_row0 + out_rows)."""
     import torch
+    if not isinstance(d_src, torch.Tensor) or d_src.dim() != 2:
+        raise InvalidArgument("band source must be a 2-D (rows, W) CUDA tensor")
+    _check_device_tensor(d_src, "band source", d_src.shape, d_src.device)
     rows, W = d_src.shape
+    _check_device_tensor(d_dst, "d_dst", (out_rows, W), d_src.device)
+    _check_fallbacks(d_fallbacks, d_src.device)
     c = _approx_args(approx)
     st = stream if stream is not None else torch.cuda.current_stream(d_src.device)
     _check(_lib.load().fbf_fast_bilateral_band_f32_device(
@@ -539,6 +602,7 @@ def fast_bilateral_band_device(d_src, src_row0: int, height: int, out_row0: int,
 def validate_device(d_img, dynamic_range: int = 255, stream=None) -> None:
     """validate_intensities (filter.cpp:19-23) on a device tensor."""
     import torch
+    _check_device_tensor(d_img, "validate_device input", d_img.shape, d_img.device)
     st = stream if stream is not None else torch.cuda.current_stream(d_img.device)
     _check(_lib.load().fbf_validate_f32_device(ctypes.c_void_p(d_img.data_ptr()), d_img.numel(), dynamic_range,
                                                d_img.device.index, ctypes.c_void_p(st.cuda_stream)))
@@ -599,8 +663,11 @@ def brute_bilateral_device(d_img, kernel: SpatialKernel, range_samples: RangeKer
                            border=BorderPolicy.symmetric, d_fallbacks=None, stream=None) -> None:
     """Device-resident brute filter: d_img float32 (H, W), d_out float64 (H, W) CUDA tensors."""
     import torch
-    if d_img.dtype != torch.float32 or d_out.dtype != torch.float64 or not d_img.is_contiguous():
-        raise InvalidArgument("brute_bilateral_device: float32 input and float64 output tensors")
+    if not isinstance(d_img, torch.Tensor) or d_img.dim() != 2:
+        raise InvalidArgument("brute_bilateral_device: float32 (H, W) input tensor")
+    _check_device_tensor(d_img, "brute_bilateral_device input", d_img.shape, d_img.device)
+    _check_device_tensor(d_out, "brute_bilateral_device output", d_img.shape, d_img.device, torch.float64)
+    _check_fallbacks(d_fallbacks, d_img.device)
     H, W = d_img.shape
     st = stream if stream is not None else torch.cuda.current_stream(d_img.device)
     _check(_lib.load().fbf_brute_bilateral_f32_device(
@@ -637,6 +704,8 @@ def compare_images_device(d_ref, d_cand, stream=None) -> ImageDelta:
     import torch
     if d_ref.shape != d_cand.shape:
         raise InvalidArgument("compare_images: dimension mismatch")
+    _check_device_tensor(d_ref, "compare_images reference", d_ref.shape, d_ref.device, torch.float64)
+    _check_device_tensor(d_cand, "compare_images candidate", d_ref.shape, d_ref.device)
     st = stream if stream is not None else torch.cuda.current_stream(d_ref.device)
     mse, psnr, mx = ctypes.c_double(0), ctypes.c_double(0), ctypes.c_double(0)
     _check(_lib.load().fbf_compare_images_device(ctypes.c_void_p(d_ref.data_ptr()), ctypes.c_void_p(d_cand.data_ptr()),
