@@ -44,7 +44,7 @@ def build_oracle(with_ref: bool | None = None) -> None:
     if with_ref is None:
         with_ref = os.path.isdir("/root/reference/proj/src")
     if with_ref:
-        targets.append("ref")
+        targets += ["ref", "integration"]
     subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
 
 
