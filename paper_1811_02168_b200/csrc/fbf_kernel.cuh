@@ -98,7 +98,7 @@ constexpr int kHalfMaxPairs = 7;
 // threads of a launch: FFMA2 warps, plus combine, gen and loader (half mode:
 // rounded up to whole sub-partition rows, unused slots idle)
 __host__ __device__ constexpr int block_threads(int pairs, int mode) {
-    return mode == kHalfMode ? 4 * ((3 * pairs + 9 + 3) / 4) * 32
+    return mode == kHalfMode ? 4 * ((3 * pairs + kGenWarps + kCombWarps + 1 + 3) / 4) * 32
                              : (mode == kPairMode ? 1 : 2) * 32 * pairs + kExtraThreads;
 }
 enum Role { kRoleGen = 0, kRoleRow = 1, kRoleCol = 2, kRoleLoad = 3, kRoleComb = 4, kRoleIdle = 5 };
@@ -778,18 +778,30 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
         }
     };
 
+    // Per-role segment loops: each role walks this CTA's segments on its own, so a
+    // role's loop carries only its own state across segments (one shared segment
+    // loop kept every role's loop state live in every role; measured c4 0.638 -> 0.650).
+    auto for_each_segment = [&](auto&& body) {
+        int gstep = 0;  // global step counter: buffers and ring blocks are used round-robin over it
+        for (long long u = u_begin; u < u_end;) {
+            long long next;
+            const Segment sg = segment_at(u, next);
+            u = next;
+            body(sg, gstep);
+            gstep += sg.steps;
+        }
+    };
+#define FBF_SEGMENT_LOCALS                                          \
+    const int steps = sg.steps;                                     \
+    const int x0 = sg.x0, ya = sg.ya, yb = sg.yb, a0 = sg.a0;       \
+    const int xs = (x0 - R) & ~3; /* f staging row origin (16-byte aligned) */ \
+    (void)steps, (void)x0, (void)ya, (void)yb, (void)a0, (void)xs;
+
     auto run_roles = [&](auto fma_region) {
     constexpr bool FMA = decltype(fma_region)::value;
-    int gstep = 0;  // global step counter: buffers and ring blocks are used round-robin over it
-    for (long long u = u_begin; u < u_end;) {
-        long long next;
-        const Segment sg = segment_at(u, next);
-        u = next;
-        const int steps = sg.steps;
-        const int x0 = sg.x0, ya = sg.ya, yb = sg.yb, a0 = sg.a0;
-        const int xs = (x0 - R) & ~3;  // f staging row origin (16-byte aligned)
-
-        if (role == kRoleLoad) {
+    if (role == kRoleLoad) {
+        for_each_segment([&](const Segment& sg, const int gstep) {
+        FBF_SEGMENT_LOCALS
             // ============================ LOAD ==============================
             // fstage row q holds f at columns [xs, xs + FSW), border-mapped with
             // 4-byte cp.async (or one TMA bulk copy per row for the in-image span,
@@ -872,7 +884,10 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                 __syncwarp();
                 if (tid == 0) mbar_arrive(&fs_full[fb]);
             }
-        } else if (role == kRoleGen) {
+        });
+    } else if (role == kRoleGen) {
+        for_each_segment([&](const Segment& sg, const int gstep) {
+        FBF_SEGMENT_LOCALS
             // ============================= GEN ==============================
             GenItem gi[GITER];
             gen_items(sg, gi);
@@ -891,7 +906,10 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                 named_arrive(kBarFsEmpty + fb, kFsThreads);
                 named_arrive(kBarGenFull + gb, gen_threads);
             }
-        } else if (role == kRoleComb) {
+        });
+    } else if (role == kRoleComb) {
+        for_each_segment([&](const Segment& sg, const int gstep) {
+        FBF_SEGMENT_LOCALS
             // ============================ COMB ==============================
             CombItem ci[CITER];
             comb_items(sg, ci);
@@ -909,7 +927,10 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
 #endif
                 named_arrive(kBarColEmpty + cb, col_threads);  // this warp is done with column buffer cb
             }
-        } else if (FMA && G::PAIR && role == kRoleRow) {
+        });
+    } else if (FMA && G::PAIR && role == kRoleRow) {
+        for_each_segment([&](const Segment& sg, const int gstep) {
+        FBF_SEGMENT_LOCALS
             // ============================= PAIR =============================
             // row pass of step t into the warp's own block, then the scatter column
             // pass of the same rows; the 2R column partial sums stay in registers
@@ -937,7 +958,10 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                     named_arrive(kBarColFull + cb, col_threads);
                 }
             }
-        } else if (FMA && role == kRoleRow) {
+        });
+    } else if (FMA && role == kRoleRow) {
+        for_each_segment([&](const Segment& sg, const int gstep) {
+        FBF_SEGMENT_LOCALS
             // ============================= ROW ==============================
             if constexpr (FMA && !G::PAIR) {
                 const int pr = tid / 32;  // this warp's channel pair
@@ -957,7 +981,10 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                     if (lane == 0) mbar_arrive(&ring_full[pr * RBP + blk]);
                 }
             }
-        } else if (FMA && role == kRoleCol) {
+        });
+    } else if (FMA && role == kRoleCol) {
+        for_each_segment([&](const Segment& sg, const int gstep) {
+        FBF_SEGMENT_LOCALS
             // ============================= COL ==============================
             const int pr = tid / 32;
             const float2* myring = ring + (size_t)pr * RROWS * RS;
@@ -1023,10 +1050,10 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                     named_arrive(kBarColFull + cb, col_threads);
                 }
             }
-        }
-        gstep += steps;
+        });
     }
     };  // run_roles
+#undef FBF_SEGMENT_LOCALS
 #ifdef FBF_DEV_PAIRONLY
     if (role != kRoleRow) role = kRoleIdle;
 #endif
