@@ -36,7 +36,7 @@ namespace fbf_dev {
 
 namespace {
 
-using LaunchFn = cudaError_t (*)(const Params&, int, cudaStream_t);
+using LaunchFn = cudaError_t (*)(const Params&, const CUtensorMap&, int, cudaStream_t);
 // One step-height variant of a radius: launchers by NKR (number of k >= 1 terms
 // in the launch) and the channel pairs that fit per CTA for each (gen buffers,
 // column buffers) choice.
@@ -426,6 +426,40 @@ void half_mode_placement(int np, fbf_dev::Params& p) {
     }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (libfbf.so does
+// not link libcuda: it must load on machines without a driver, and the filter
+// then fails with FBF_ECUDA).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// The source of a job as a 3-D tensor (columns, rows present, frames) with a box of
+// one f staging tile: FSW = the kernel's staged row width, Q rows, one frame.
+int encode_source_map(const Job& job, int r, int q, CUtensorMap* map) {
+    static EncodeTiledFn enc = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &qr) !=
+                cudaSuccess || qr != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            fn = nullptr;
+        }
+        return (EncodeTiledFn)fn;
+    }();
+    if (!enc) return fail(FBF_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const int gw = kTW + 2 * r, fsw = (gw + 3 + 3) / 4 * 4;  // Geometry::FSW
+    cuuint64_t dims[3] = {(cuuint64_t)job.width, (cuuint64_t)job.src_rows, (cuuint64_t)job.n_frames};
+    cuuint64_t strides[2] = {(cuuint64_t)job.width * sizeof(float),
+                             (cuuint64_t)(job.n_frames > 1 ? job.src_frame_stride : (long long)job.width * job.src_rows) *
+                                 sizeof(float)};
+    cuuint32_t box[3] = {(cuuint32_t)fsw, (cuuint32_t)q, 1}, es[3] = {1, 1, 1};
+    const CUresult rc = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(job.d_src), dims, strides, box,
+                            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS) return fail(FBF_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)rc));
+    return FBF_OK;
+}
+
 // Runs every chunk launch for one job on `stream`. `scratch` must hold
 // n_frames * out_rows * width float2 when K needs more than one chunk.
 int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int border,
@@ -436,8 +470,17 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
     const Plan plan = make_plan(a.K, r, units < 64LL * ctx.num_sms);
     if (!plan.ent) return fail(FBF_ECAPACITY, "no kernel variant fits the shared memory for this radius");
     if (plan.chunks.size() > 1 && !scratch) return fail(FBF_EINVAL, "internal: scratch required");
+    static const bool log_plan = std::getenv("FBF_PLAN_LOG") != nullptr;  // dev: print the launch plan
+    if (log_plan) {
+        std::string line = "fbf plan: K=" + std::to_string(a.K) + " r=" + std::to_string(r) + " mode=" +
+                           std::to_string(plan.mode) + " Q=" + std::to_string(plan.q) + " ngb=" +
+                           std::to_string(plan.ngb) + " ncb=" + std::to_string(plan.ncb) + " chunks:";
+        for (const Chunk& c : plan.chunks) line += " " + std::to_string(c.n_pairs);
+        std::fprintf(stderr, "%s units=%lld\n", line.c_str(), units);
+    }
 
     fbf_dev::Params p{};
+    CUtensorMap tmap{};
     p.src = job.d_src;
     p.src_frame_stride = job.src_frame_stride;
     p.src_pitch = job.width;
@@ -466,14 +509,24 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
     // Interior f rows: element cp.async by default (measured fastest on B200:
     // profiles/r01_stage_modes.txt); FBF_STAGE=bulk routes them through the TMA
     // bulk-copy engine (needs 16-byte aligned rows).
+    // FBF_STAGE (dev): "tma" (default) interior tiles by 2-D tensor-map TMA, "elem"
+    // element / 16-byte cp.async only, "bulk" 1-D bulk copies per row
     static const int stage_mode = [] {
         const char* e = std::getenv("FBF_STAGE");
-        return e && std::strcmp(e, "bulk") == 0 ? 1 : 0;
+        if (e && std::strcmp(e, "bulk") == 0) return 1;
+        if (e && std::strcmp(e, "elem") == 0) return 2;
+        return 0;
     }();
     const bool aligned = job.width % 4 == 0 && ((uintptr_t)job.d_src & 15) == 0 &&
                          (job.n_frames == 1 || job.src_frame_stride % 4 == 0);
-    p.use_tma = aligned ? stage_mode : 0;
+    p.use_tma = aligned && stage_mode == 1 ? 1 : 0;
     p.vec_ok = aligned ? 1 : 0;
+    p.use_tma2d = 0;
+    if (aligned && stage_mode == 0) {
+        const int rc = encode_source_map(job, r, plan.q, &tmap);
+        if (rc != FBF_OK) return rc;
+        p.use_tma2d = 1;
+    }
     // persistent grid: CTAs per SM x SMs, but keep segments at least a few steps long
     p.ngb = plan.ngb;
     p.prof = dev_prof_buffer();
@@ -494,7 +547,7 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
         p.inv_period = a.turns();
         p.k_first = std::max(c.k_lo, 1);
         if (plan.mode == fbf_dev::kHalfMode) half_mode_placement(c.n_pairs, p);
-        const cudaError_t e = plan.ent->launch[nkr](p, grid, stream);
+        const cudaError_t e = plan.ent->launch[nkr](p, tmap, grid, stream);
         if (e != cudaSuccess) return cuda_fail(e, "fbf_fused_kernel launch");
         g_launches.fetch_add(1, std::memory_order_relaxed);
     }

@@ -41,6 +41,7 @@
 //     float2 scratch image between passes, still in ascending k.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (type only; the map is encoded on the host)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -138,6 +139,7 @@ struct Params {
     unsigned long long* prof;    // dev builds with FBF_PHASES: per warp slot [total, wait A, wait B, CTAs] cycles
     unsigned char warp_role[32]; // half mode: Role and role index of every warp slot
     unsigned char warp_idx[32];
+    int use_tma2d;               // interior f tiles by the tensor map (kernel parameter `tmap`)
 };
 
 #ifdef FBF_PHASES
@@ -344,6 +346,17 @@ __device__ __forceinline__ int lane_id_() { return (int)(threadIdx.x & 31); }
 // barrier ids (0 is __syncthreads): gen full/empty, column full/empty, f stage empty
 constexpr int kBarGenFull = 1, kBarGenEmpty = 3, kBarColFull = 5, kBarColEmpty = 7, kBarFsEmpty = 9;
 
+// 2-D tile of the 3-D tensor map (box FSW x Q x 1 at columns x.., rows y.. of frame
+// z) into shared memory, completion on `bar` (coordinates outside the map fill 0).
+__device__ __forceinline__ void tma_tile_g2s(float* smem_dst, const CUtensorMap* map, int x, int y, int z,
+                                             uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // 1-D TMA bulk copy global -> shared (16-byte aligned, size multiple of 16),
 // completion on `bar`.
 __device__ __forceinline__ void tma_bulk_g2s(float* smem_dst, const float* gsrc, unsigned bytes, uint64_t* bar) {
@@ -484,7 +497,11 @@ struct Segment {
 // full/empty mbarrier pairs with per-warp arrivals:
 //   LOAD -fs-> GEN -gen-> ROW p -ring p-> COL p -col-> COMB
 template <int R, int Q, int NKR, int M>
-__global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_kernel(const __grid_constant__ Params p) {
+// `tmap`: 3-D tensor map over the source (columns, rows present in src, frames)
+// with a box of one f tile (FSW, Q, 1) -- a kernel parameter of its own (its
+// address is taken for the TMA; inside Params that made ptxas spill the FFMA2 loops).
+__global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
+    fbf_fused_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmap) {
     using G = Geometry<R, Q, M>;
     constexpr int GW = G::GW, GS = G::GS, FSW = G::FSW, RB = G::RB, RBP = G::RBP, RROWS = G::RROWS, RS = G::RS;
     constexpr int NFS = G::NFS;
@@ -701,17 +718,28 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
     };
     // f of the step's output pixels, loaded before the step's column results are
     // waited for so that the L2 latency overlaps the wait
-    auto combine_load = [&](const Segment& sg, const CombItem (&ci)[CITER], float2 (&fv)[CITER]) {
+    // (and, after the first coefficient chunk, the (num, den) carried in the scratch
+    // image: an HBM read whose latency otherwise stalls the step, c2 0.585 -> 0.595)
+    auto combine_load = [&](const Segment& sg, const CombItem (&ci)[CITER], float2 (&fv)[CITER],
+                            float4 (&nd)[CITER]) {
 #pragma unroll
         for (int it = 0; it < CITER; ++it) {
             fv[it] = make_float2(0.f, 0.f);
-            if (ci[it].y < sg.yb && ci[it].colok) fv[it] = make_float2(__ldg(ci[it].sp), ci[it].vb ? __ldg(ci[it].sp + 1) : 0.f);
+            nd[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (ci[it].y < sg.yb && ci[it].colok) {
+                fv[it] = make_float2(__ldg(ci[it].sp), ci[it].vb ? __ldg(ci[it].sp + 1) : 0.f);
+                if (!p.first_chunk) {
+                    const float2 a = __ldcg(ci[it].ap), b = ci[it].vb ? __ldcg(ci[it].ap + 1) : make_float2(0.f, 0.f);
+                    nd[it] = make_float4(a.x, b.x, a.y, b.y);  // (num a, num b, den a, den b)
+                }
+            }
         }
     };
     // per-step pointer advances (64-bit adds, no wide multiplies in the step loop)
     const long long src_step = (long long)Q * p.src_pitch, dst_step = (long long)Q * p.dst_pitch,
                     acc_step = (long long)Q * p.width;
-    auto combine_step = [&](const Segment& sg, int cb, CombItem (&ci)[CITER], const float2 (&fv)[CITER]) {
+    auto combine_step = [&](const Segment& sg, int cb, CombItem (&ci)[CITER], const float2 (&fv)[CITER],
+                            const float4 (&nd)[CITER]) {
         const float* cbase = reinterpret_cast<const float*>(colout + cb * np * Q * kTW);
         const bool kfirst_c = p.k_first > 1;
 #pragma unroll
@@ -725,9 +753,8 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                     atomicOr(p.bad_pixels, 1u);
                 float2 num = make_float2(0.f, 0.f), den = make_float2(0.f, 0.f);
                 if (!p.first_chunk) {
-                    const float2 nda = c.ap[0], ndb = vb ? c.ap[1] : make_float2(0.f, 0.f);
-                    num = make_float2(nda.x, ndb.x);
-                    den = make_float2(nda.y, ndb.y);
+                    num = make_float2(nd[it].x, nd[it].y);
+                    den = make_float2(nd[it].z, nd[it].w);
                 }
                 // planar column results [pair][channel][q][TW]: float2 = the two pixels of one channel
                 const float2* go = reinterpret_cast<const float2*>(cbase + c.co);
@@ -839,6 +866,19 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                 if (tid == 0) mbar_arrive(&fs_full[fb]);
                 continue;
 #endif
+                // interior step (every row in the image, the window inside the row): one
+                // tensor-map TMA of the whole Q x FSW tile. Rows the band's source window
+                // lacks are outside the map (zero fill); they feed no stored output.
+#ifndef FBF_NO_TMA2D
+                if (p.use_tma2d && xs >= 0 && xs + FSW <= p.width && a >= 0 && a + Q <= p.height) {
+                    if (tid == 0) {
+                        mbar_expect_tx(&fs_full[fb], (unsigned)(sizeof(float) * Q * FSW));
+                        tma_tile_g2s(fs, &tmap, xs, a - p.src_row0, sg.frame, &fs_full[fb]);
+                        mbar_arrive(&fs_full[fb]);
+                    }
+                    continue;
+                }
+#endif
                 if (vec) {
                     constexpr int NV = FSW / 4;  // float4 per staged row
                     constexpr int VITER = (Q * NV + 31) / 32;
@@ -917,13 +957,14 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1) fbf_fused_ke
                 const int g = gstep + t;
                 const int cb = (g & (ncb - 1));
                 float2 fv[CITER];
-                if (t >= s0) combine_load(sg, ci, fv);
+                float4 nd[CITER];
+                if (t >= s0) combine_load(sg, ci, fv, nd);
                 PSYNC(0, kBarColFull + cb, col_threads);
 #ifndef FBF_SKIP_COMB
 #ifdef FBF_DEV_LIGHT_W0
                 if (tid < 32)
 #endif
-                if (t >= s0) combine_step(sg, cb, ci, fv);
+                if (t >= s0) combine_step(sg, cb, ci, fv, nd);
 #endif
                 named_arrive(kBarColEmpty + cb, col_threads);  // this warp is done with column buffer cb
             }
@@ -1095,7 +1136,7 @@ roles_done:
 }
 
 template <int R, int Q, int NKR, int M>
-cudaError_t launch_fused(const Params& p, int grid, cudaStream_t stream) {
+cudaError_t launch_fused(const Params& p, const CUtensorMap& tmap, int grid, cudaStream_t stream) {
     using G = Geometry<R, Q, M>;
     const size_t smem = G::smem_bytes(p.n_pairs, p.ngb, p.ncb);
     // The dynamic shared-memory opt-in is a property of the function in the
@@ -1113,7 +1154,7 @@ cudaError_t launch_fused(const Params& p, int grid, cudaStream_t stream) {
         if (e != cudaSuccess) return e;
         configured.fetch_or(bit, std::memory_order_acq_rel);
     }
-    fbf_fused_kernel<R, Q, NKR, M><<<grid, block_threads(p.n_pairs, M), smem, stream>>>(p);
+    fbf_fused_kernel<R, Q, NKR, M><<<grid, block_threads(p.n_pairs, M), smem, stream>>>(p, tmap);
     return cudaGetLastError();
 }
 
