@@ -534,6 +534,26 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
     const long long min_seg = 4 * plan.q;
     const long long want = (p.total_units + min_seg - 1) / min_seg;
     const int grid = (int)std::max(1LL, std::min<long long>((long long)ctx.num_sms, want));
+    // Whole columns (frame, strip) round-robin over the CTAs first: neighbouring strips
+    // stream the same rows at the same time, so the halo columns they share are read
+    // from DRAM once (c4: 3.24 -> 1.26 GB read per launch for a 1.07 GB input, time
+    // unchanged); then a contiguous split of the rest. FBF_ORDER=contig (dev): the
+    // plain contiguous split.
+    static const bool contig = [] {
+        const char* e = std::getenv("FBF_ORDER");
+        return e && std::strcmp(e, "contig") == 0;
+    }();
+    p.col_rounds = contig ? 0 : (int)(((long long)job.n_frames * p.n_strips) / grid);
+    // Programmatic dependent launch for short launches (< 1024 output rows per CTA: the
+    // next grid's launch and prologue overlap this one's drain): c0 24.8 -> 24.0 us,
+    // one c3 frame 0.499 -> 0.513. Long launches lose with it (c4 0.701 -> 0.693, c2
+    // 0.599 -> 0.591: the dependent grid's CTAs land on SMs in drain order, not launch
+    // order). FBF_PDL=0 / 1 (dev) forces it off / on.
+    static const int pdl_env = [] {
+        const char* v = std::getenv("FBF_PDL");
+        return v ? std::atoi(v) : -1;
+    }();
+    p.pdl = pdl_env >= 0 ? pdl_env : (p.total_units < 1024LL * grid ? 1 : 0);
 
     for (size_t ci = 0; ci < plan.chunks.size(); ++ci) {
         const Chunk& c = plan.chunks[ci];

@@ -140,6 +140,8 @@ struct Params {
     unsigned char warp_role[32]; // half mode: Role and role index of every warp slot
     unsigned char warp_idx[32];
     int use_tma2d;               // interior f tiles by the tensor map (kernel parameter `tmap`)
+    int col_rounds;              // whole columns (frame, strip) per CTA taken round-robin before the tail
+    int pdl;                     // host: launch with programmatic stream serialization
 };
 
 #ifdef FBF_PHASES
@@ -345,6 +347,12 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 __device__ __forceinline__ int lane_id_() { return (int)(threadIdx.x & 31); }
 // barrier ids (0 is __syncthreads): gen full/empty, column full/empty, f stage empty
 constexpr int kBarGenFull = 1, kBarGenEmpty = 3, kBarColFull = 5, kBarColEmpty = 7, kBarFsEmpty = 9;
+// ROW -> COL ring handoff of the half-mode rings (two blocks): one CTA-wide named
+// barrier per ring block and direction, all pairs together (the ROW warps of all
+// pairs do equal work). Per-pair mbarriers made the waiting COL warps poll: on c4
+// their try_wait retry loop was 12 % of all issued instructions, issue slots the
+// FFMA2 warps of the same sub-partition lost (c4 0.690 -> 0.703).
+constexpr int kBarRingFull = 12, kBarRingEmpty = 14;
 
 // 2-D tile of the 3-D tensor map (box FSW x Q x 1 at columns x.., rows y.. of frame
 // z) into shared memory, completion on `bar` (coordinates outside the map fill 0).
@@ -552,6 +560,12 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
     const int gen_threads = kGenThreads + nrole;   // GEN -> ROW/PAIR and back
     const int col_threads = (M == kHalfMode ? 2 : 1) * nrole + kCombThreads;  // COL/PAIR -> COMB and back
     constexpr int kFsThreads = kGenThreads + 32;   // GEN -> LOAD (f stage empty)
+    // half-mode rings (two blocks) hand over through named barriers (ROW + COL threads
+    // of all pairs). Split mode keeps the per-pair mbarriers: its 9-pair launches (c3)
+    // measured 0.493 -> 0.489 with the CTA-wide barrier (the pairs lockstep).
+    constexpr bool RING_NB = M == kHalfMode && RBP == 2;
+    static_assert(kBarFsEmpty + NFS <= kBarRingFull, "named barrier ids overlap");
+    const int ring_threads = (M == kHalfMode ? 3 : 2) * nrole;
 #ifdef FBF_PHASES
     long long _pw[2] = {0, 0};
     const long long _pt0 = clock64();
@@ -566,24 +580,36 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
+    // Programmatic dependent launch: this grid may start while the previous kernel on
+    // the stream drains (its CTAs free SMs at different times). Wait for that grid and
+    // its memory (the previous chunk's (num, den) scratch, a caller's producer kernel)
+    // before any global access, then let the next launch begin its own prologue.
+    // Without the launch attribute both instructions are no-ops.
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
-    // this CTA's contiguous share of the (frame, strip, row) units
+    // This CTA's work: `col_rounds` whole columns (frame, strip) taken round-robin --
+    // column j * gridDim.x + blockIdx.x in round j, so at any time the CTAs stream
+    // neighbouring strips over the same rows and the halo columns two strips share
+    // are read from DRAM once (L2 hits for the second) -- then a contiguous share of
+    // the remaining (frame, strip, row) units.
     const long long U = p.total_units;
-    const long long u_begin = U * blockIdx.x / gridDim.x;
-    const long long u_end = U * (blockIdx.x + 1) / gridDim.x;
+    const long long tail0 = (long long)p.col_rounds * gridDim.x * p.out_rows;  // first unit of the tail
+    const long long u_begin = tail0 + (U - tail0) * blockIdx.x / gridDim.x;
+    const long long u_end = tail0 + (U - tail0) * (blockIdx.x + 1) / gridDim.x;
     const long long per_frame = (long long)p.n_strips * p.out_rows;
     // steps start e rows early so that output rows begin exactly at ya; the first
     // s0 steps of a segment only fill the ring
     constexpr int e = (Q - (2 * R) % Q) % Q;
     constexpr int s0 = (2 * R + e) / Q;
     static_assert(s0 == RB - 1, "warm-up steps fill all but one ring block");
-    auto segment_at = [&](long long u, long long& next) {
+    auto segment_at = [&](long long u, long long uend, long long& next) {
         Segment sg;
         sg.frame = (int)(u / per_frame);
         const long long rem = u % per_frame;
         const int strip = (int)(rem / p.out_rows);
         const int row = (int)(rem % p.out_rows);
-        const int len = (int)min((long long)(p.out_rows - row), u_end - u);
+        const int len = (int)min((long long)(p.out_rows - row), uend - u);
         next = u + len;
         sg.x0 = strip * kTW;
         sg.ya = p.out_row0 + row;
@@ -810,10 +836,21 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
     // loop kept every role's loop state live in every role; measured c4 0.638 -> 0.650).
     auto for_each_segment = [&](auto&& body) {
         int gstep = 0;  // global step counter: buffers and ring blocks are used round-robin over it
-        for (long long u = u_begin; u < u_end;) {
-            long long next;
-            const Segment sg = segment_at(u, next);
-            u = next;
+        int j = 0;      // round of the whole-column part
+        for (long long u = u_begin;;) {
+            // one call site of `body` (two loops would inline every role twice)
+            long long next, a, b;
+            if (j < p.col_rounds) {
+                a = ((long long)j++ * gridDim.x + blockIdx.x) * p.out_rows;
+                b = a + p.out_rows;
+            } else if (u < u_end) {
+                a = u;
+                b = u_end;
+            } else {
+                break;
+            }
+            const Segment sg = segment_at(a, b, next);
+            if (a == u) u = next;
             body(sg, gstep);
             gstep += sg.steps;
         }
@@ -1014,12 +1051,16 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                     const int gb = (g & (ngb - 1)), blk = g % RBP;
                     PSYNC(0, kBarGenFull + gb, gen_threads);
                     // ring block blk last held step g - RBP, read up to column pass g - RBP + RBN - 1
-                    if (g >= RBP) PWAIT(1, &ring_empty[pr * RBP + blk], (unsigned)((g / RBP - 1) & 1));
+                    if (g >= RBP) {
+                        if constexpr (RING_NB) PSYNC(1, kBarRingEmpty + blk, ring_threads);
+                        else PWAIT(1, &ring_empty[pr * RBP + blk], (unsigned)((g / RBP - 1) & 1));
+                    }
                     const float4* gin = reinterpret_cast<const float4*>(gen + (((size_t)gb * np + pr) * Q + q) * GS + xc * Q);
                     float2* hout = myring + ((size_t)blk * Q + q) * RS + xc * Q;
                     row_pass<R, Q>(gin, hout, p, kBarGenEmpty + gb, gen_threads);
                     __syncwarp();  // ring block complete
-                    if (lane == 0) mbar_arrive(&ring_full[pr * RBP + blk]);
+                    if constexpr (RING_NB) named_arrive(kBarRingFull + blk, ring_threads);
+                    else if (lane == 0) mbar_arrive(&ring_full[pr * RBP + blk]);
                 }
             }
         });
@@ -1039,14 +1080,15 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                 for (int t = 0; t < steps; ++t) {
                     const int g = gstep + t;
                     const int blk = g % RBP, cb = (g & (ncb - 1));
-                    PWAIT(0, &ring_full[pr * RBP + blk], (unsigned)((g / RBP) & 1));
+                    if constexpr (RING_NB) PSYNC(0, kBarRingFull + blk, ring_threads);  // always: two blocks
+                    else PWAIT(0, &ring_full[pr * RBP + blk], (unsigned)((g / RBP) & 1));
                     if (g >= ncb) PSYNC(1, kBarColEmpty + cb, col_threads);
                     float* oc = reinterpret_cast<float*>(colout + ((size_t)cb * np + pr) * Q * kTW) + lane;
                     const float2* hin = hring + (size_t)blk * Q * RS + lane;
                     if (h == 0) col_scatter_half<R, Q, 0>(hin, st, oc, t >= s0, p);
                     else col_scatter_half<R, Q, 1>(hin, st, oc, t >= s0, p);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&ring_empty[pr * RBP + blk]);  // block free for row pass g + RBP
+                    if constexpr (RING_NB) named_arrive(kBarRingEmpty + blk, ring_threads);  // block free for row pass g + RBP
+                    else if (__syncwarp(), lane == 0) mbar_arrive(&ring_empty[pr * RBP + blk]);
                     named_arrive(kBarColFull + cb, col_threads);
                 }
             } else if constexpr (G::SCATTER) {
@@ -1056,14 +1098,15 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                 for (int t = 0; t < steps; ++t) {
                     const int g = gstep + t;
                     const int blk = g % RBP, cb = (g & (ncb - 1));
-                    PWAIT(0, &ring_full[pr * RBP + blk], (unsigned)((g / RBP) & 1));
+                    if constexpr (RING_NB) PSYNC(0, kBarRingFull + blk, ring_threads);  // always: two blocks
+                    else PWAIT(0, &ring_full[pr * RBP + blk], (unsigned)((g / RBP) & 1));
                     // column buffer cb must have been consumed by COMB even on warm-up steps:
                     // the arrival below completes a phase of col_full[cb]
                     if (g >= ncb) PSYNC(1, kBarColEmpty + cb, col_threads);
                     col_scatter<R, Q>(myring + (size_t)blk * Q * RS + lane, st,
                                       reinterpret_cast<float*>(colout + ((size_t)cb * np + pr) * Q * kTW) + lane, t >= s0, p);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&ring_empty[pr * RBP + blk]);  // block free for row pass g + RBP
+                    if constexpr (RING_NB) named_arrive(kBarRingEmpty + blk, ring_threads);  // block free for row pass g + RBP
+                    else if (__syncwarp(), lane == 0) mbar_arrive(&ring_empty[pr * RBP + blk]);
                     named_arrive(kBarColFull + cb, col_threads);
                 }
             } else {
@@ -1154,7 +1197,22 @@ cudaError_t launch_fused(const Params& p, const CUtensorMap& tmap, int grid, cud
         if (e != cudaSuccess) return e;
         configured.fetch_or(bit, std::memory_order_acq_rel);
     }
-    fbf_fused_kernel<R, Q, NKR, M><<<grid, block_threads(p.n_pairs, M), smem, stream>>>(p, tmap);
+    // programmatic stream serialization (host's choice, Params::pdl): the launch may
+    // begin while the previous kernel on the stream finishes; the kernel waits for it
+    // (griddepcontrol.wait) before touching global memory
+    const bool pdl = p.pdl != 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block_threads(p.n_pairs, M));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    e = cudaLaunchKernelEx(&cfg, fbf_fused_kernel<R, Q, NKR, M>, p, tmap);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
