@@ -47,6 +47,7 @@ struct QEntry {
 struct RadiusEntry {
     QEntry split8;          // split mode, Q = 8 (every radius)
     QEntry half8;           // half mode, Q = 8 (every radius, <= 7 pairs)
+    QEntry half8wg;         // half mode with the warpgroup register split (5 pairs, NKR = 2 only)
     QEntry pair8, pair16;   // pair mode, r <= kQ16MaxRadius
 };
 
@@ -58,10 +59,10 @@ QEntry qentry() {
     e.launch[1] = &launch_fused<R, Q, 1, M>;
     e.launch[2] = &launch_fused<R, Q, 2, M>;
     e.launch[3] = &launch_fused<R, Q, 3, M>;
-    if constexpr (M != kHalfMode) e.launch[4] = &launch_fused<R, Q, 4, M>;
+    if constexpr (!is_half(M)) e.launch[4] = &launch_fused<R, Q, 4, M>;
     for (int ngb = 1; ngb <= 2; ++ngb)
         for (int ncb = 1; ncb <= 2; ++ncb)
-            e.max_pairs[ngb][ncb] = M == kHalfMode ? std::min(kHalfMaxPairs, G::max_pairs(ngb, ncb))
+            e.max_pairs[ngb][ncb] = is_half(M) ? std::min(kHalfMaxPairs, G::max_pairs(ngb, ncb))
                                                    : G::max_pairs(ngb, ncb);
     return e;
 }
@@ -74,6 +75,9 @@ RadiusEntry entry() {
 #endif
     e.split8 = qentry<R, 8, kSplitMode>();
     e.half8 = qentry<R, 8, kHalfMode>();
+    e.half8wg = e.half8;
+    e.half8wg.launch[0] = e.half8wg.launch[1] = e.half8wg.launch[3] = nullptr;
+    e.half8wg.launch[2] = &launch_fused<R, 8, 2, kHalfWgMode>;
     if constexpr (R <= kQ16MaxRadius) {
         e.pair8 = qentry<R, 8, kPairMode>();
         e.pair16 = qentry<R, 16, kPairMode>();
@@ -262,6 +266,7 @@ struct Plan {
     std::vector<Chunk> chunks;
     int q = 8, mode = 1, ngb = 2, ncb = 2;
     const fbf_dev::QEntry* ent = nullptr;
+    const fbf_dev::QEntry* ent_wg = nullptr;  // half mode: the warpgroup-split variant (5 pairs)
 };
 
 // Split k = 0..K-1 into launches whose channel pairs fit in shared memory
@@ -356,7 +361,7 @@ Plan make_plan(int K, int r, bool short_work = false) {
                 if (cand16 != best16) better = cand16;
             }
             if (better) {
-                best = Plan{std::move(chunks), pf.q, pf.mode, pf.ngb, pf.ncb, qe};
+                best = Plan{std::move(chunks), pf.q, pf.mode, pf.ngb, pf.ncb, qe, pf.mode == H ? &ent.half8wg : nullptr};
                 best_bal = bal;
             }
         }
@@ -389,9 +394,28 @@ struct Job {
 // spread evenly (ROW warps weigh 2, each COL half 1), the light roles by their
 // estimated issue load; within a sub-partition the FFMA2 warps take the highest
 // warp ids (the issue arbiter serves higher ids first), unused slots idle.
-void half_mode_placement(int np, fbf_dev::Params& p) {
+// Returns true when it wrote the fixed warpgroup layout of the kHalfWgMode kernel.
+bool half_mode_placement(int np, fbf_dev::Params& p) {
     using namespace fbf_dev;
     const int W = block_threads(np, kHalfMode) / 32, per = W / 4;
+    // 5 pairs (c4): a fixed warpgroup layout for the kernel's register split -- gen and
+    // combine in warpgroups 0-1 (64 registers), loader + ROW + COL halves in 2-5 (88).
+    // FFMA2 weight per sub-partition (warp id mod 4; ROW 2, COL half 1): 5 5 5 5.
+    static const bool no_split = std::getenv("FBF_HALF_SPLIT") && std::atoi(std::getenv("FBF_HALF_SPLIT")) == 0;
+    if (np == 5 && W == 24 && !no_split) {
+        static const unsigned char role[24] = {kRoleGen, kRoleGen, kRoleGen, kRoleGen,      // WG0
+                                               kRoleComb, kRoleComb, kRoleComb, kRoleComb,  // WG1
+                                               kRoleLoad, kRoleCol, kRoleCol, kRoleCol,     // WG2
+                                               kRoleCol, kRoleCol, kRoleCol, kRoleCol,      // WG3
+                                               kRoleRow, kRoleCol, kRoleCol, kRoleCol,      // WG4
+                                               kRoleRow, kRoleRow, kRoleRow, kRoleRow};     // WG5
+        int next[6] = {0, 0, 0, 0, 0, 0};
+        for (int w = 0; w < 32; ++w) {
+            p.warp_role[w] = w < 24 ? role[w] : (unsigned char)kRoleIdle;
+            p.warp_idx[w] = w < 24 ? (unsigned char)next[role[w]]++ : 0;
+        }
+        return true;
+    }
     struct Item {
         int role, idx;
         double w;
@@ -424,6 +448,7 @@ void half_mode_placement(int np, fbf_dev::Params& p) {
             p.warp_idx[s + 4 * k] = (unsigned char)it.idx;
         }
     }
+    return false;
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (libfbf.so does
@@ -566,8 +591,9 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
         for (int kk = 0; kk < c.n_k; ++kk) p.coeff[kk] = (float)a.c[c.k_lo + kk];
         p.inv_period = a.turns();
         p.k_first = std::max(c.k_lo, 1);
-        if (plan.mode == fbf_dev::kHalfMode) half_mode_placement(c.n_pairs, p);
-        const cudaError_t e = plan.ent->launch[nkr](p, tmap, grid, stream);
+        const bool wg = plan.mode == fbf_dev::kHalfMode && half_mode_placement(c.n_pairs, p);
+        const fbf_dev::QEntry* qe = wg ? plan.ent_wg : plan.ent;  // every radius has the split variant
+        const cudaError_t e = qe->launch[nkr](p, tmap, grid, stream);
         if (e != cudaSuccess) return cuda_fail(e, "fbf_fused_kernel launch");
         g_launches.fetch_add(1, std::memory_order_relaxed);
     }

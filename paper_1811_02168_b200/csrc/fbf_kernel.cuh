@@ -83,7 +83,10 @@ constexpr size_t kSmemReservedPerBlock = 1024;
 //               3 np FFMA2 warps have weights 2:1:1, which the host places on
 //               the sub-partitions so that each gets the same FFMA2 work
 //               (Params::warp_role), for up to 7 pairs per launch.
-constexpr int kPairMode = 0, kSplitMode = 1, kHalfMode = 2;
+//   kHalfWgMode: half mode with a fixed warpgroup layout and a setmaxnreg register
+//               split (5 pairs, 24 warps; NKR = 2 only), see the kernel tail.
+constexpr int kPairMode = 0, kSplitMode = 1, kHalfMode = 2, kHalfWgMode = 3;
+__host__ __device__ constexpr bool is_half(int mode) { return mode == kHalfMode || mode == kHalfWgMode; }
 // Pair mode with 7 pairs (16 warps): warpgroups 2-3 (7 pair warps + loader) run at
 // FBF_REGSPLIT_HI registers, warpgroups 0-1 (gen + combine) at FBF_REGSPLIT_LO
 // (setmaxnreg; 8 x LO + 8 x HI = 16 x 128). Measured on c1: 96/160 0.571 of the
@@ -99,7 +102,7 @@ constexpr int kHalfMaxPairs = 7;
 // threads of a launch: FFMA2 warps, plus combine, gen and loader (half mode:
 // rounded up to whole sub-partition rows, unused slots idle)
 __host__ __device__ constexpr int block_threads(int pairs, int mode) {
-    return mode == kHalfMode ? 4 * ((3 * pairs + kGenWarps + kCombWarps + 1 + 3) / 4) * 32
+    return is_half(mode) ? 4 * ((3 * pairs + kGenWarps + kCombWarps + 1 + 3) / 4) * 32
                              : (mode == kPairMode ? 1 : 2) * 32 * pairs + kExtraThreads;
 }
 enum Role { kRoleGen = 0, kRoleRow = 1, kRoleCol = 2, kRoleLoad = 3, kRoleComb = 4, kRoleIdle = 5 };
@@ -174,7 +177,7 @@ struct Geometry {
     // live in registers ("scatter": every row-pass output is read once), so the
     // ring is just a double buffer of Q rows; larger radii gather a window of
     // ring rows (RB blocks) per step.
-    static constexpr bool SCATTER = R <= 16 || M == kHalfMode;
+    static constexpr bool SCATTER = R <= 16 || is_half(M);
     static_assert(SCATTER || !PAIR, "pair mode keeps the column partial sums in registers");
     static constexpr int RB = 1 + (2 * R + Q - 1) / Q;           // ring blocks a gather column pass reads
     static constexpr int RBN = SCATTER ? 1 : RB;                 // blocks a column pass reads
@@ -527,7 +530,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
     const int nrole = np * 32;  // threads of the ROW/PAIR role (and of the COL role in split mode)
     const int nf = G::PAIR ? nrole : 2 * nrole;  // FFMA2 threads
     int role, tid;  // Role; ROW is PAIR in pair mode
-    if constexpr (M == kHalfMode) {
+    if constexpr (is_half(M)) {
         const int w = (int)(threadIdx.x / 32);
         role = p.warp_role[w];
         tid = p.warp_idx[w] * 32 + (int)(threadIdx.x & 31);
@@ -558,14 +561,14 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
     const int zk = p.k_lo == 0 ? 1 : 0;  // k = 0 contributes the single pair (f, 1)
     // named-barrier thread counts: producers + consumers of each handoff
     const int gen_threads = kGenThreads + nrole;   // GEN -> ROW/PAIR and back
-    const int col_threads = (M == kHalfMode ? 2 : 1) * nrole + kCombThreads;  // COL/PAIR -> COMB and back
+    const int col_threads = (is_half(M) ? 2 : 1) * nrole + kCombThreads;  // COL/PAIR -> COMB and back
     constexpr int kFsThreads = kGenThreads + 32;   // GEN -> LOAD (f stage empty)
     // half-mode rings (two blocks) hand over through named barriers (ROW + COL threads
     // of all pairs). Split mode keeps the per-pair mbarriers: its 9-pair launches (c3)
     // measured 0.493 -> 0.489 with the CTA-wide barrier (the pairs lockstep).
-    constexpr bool RING_NB = M == kHalfMode && RBP == 2;
+    constexpr bool RING_NB = is_half(M) && RBP == 2;
     static_assert(kBarFsEmpty + NFS <= kBarRingFull, "named barrier ids overlap");
-    const int ring_threads = (M == kHalfMode ? 3 : 2) * nrole;
+    const int ring_threads = (is_half(M) ? 3 : 2) * nrole;
 #ifdef FBF_PHASES
     long long _pw[2] = {0, 0};
     const long long _pt0 = clock64();
@@ -575,7 +578,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
         for (int b = 0; b < NFS; ++b) mbar_init(&fs_full[b], 1);
         for (int b = 0; b < np * RBP; ++b) {
             mbar_init(&ring_full[b], 1);
-            mbar_init(&ring_empty[b], M == kHalfMode ? 2 : 1);  // both COL halves release a block
+            mbar_init(&ring_empty[b], is_half(M) ? 2 : 1);  // both COL halves release a block
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -1071,7 +1074,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
             const int pr = tid / 32;
             const float2* myring = ring + (size_t)pr * RROWS * RS;
             if constexpr (!FMA || G::PAIR) {
-            } else if constexpr (M == kHalfMode) {
+            } else if constexpr (is_half(M)) {
                 const int pr = tid / 64, h = (tid / 32) & 1;  // pair, output-row parity
                 const float2* hring = ring + (size_t)pr * RROWS * RS;
                 float2 st[R];
@@ -1142,11 +1145,25 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
     if (role != kRoleRow) role = kRoleIdle;
 #endif
 #ifndef FBF_NO_REGSPLIT
-    // Register split between warpgroups (pair mode, 7 pairs, 16 warps): warpgroups
-    // 0-1 (loader, gen, 3 combine warps) give up registers, 2-3 (7 pair warps +
-    // one combine warp) take them, so the pair warps' row pass can keep loads in
-    // flight next to the 2r live column partial sums. 8 x 96 + 8 x 160 = 16 x 128.
-    if constexpr (M == kPairMode && NKR == 3) {
+    if constexpr (M == kHalfWgMode) {
+        // Half mode, 5 pairs, 24 warps (c4): the host places gen + combine in
+        // warpgroups 0-1 (64 registers) and loader, ROW and COL-half warps in 2-5 (88):
+        // at the uniform 80 the COL halves (R float2 partial sums) spill their loop
+        // state around every step. 8 x 64 + 16 x 88 = 24 x 80. Its own instantiation:
+        // a second, unsplit copy of the roles in the same function made ptxas spill
+        // the COL loops of both copies.
+        if (threadIdx.x < 256) {
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n");
+            if (role != kRoleIdle) run_roles(std::false_type{});
+        } else {
+            asm volatile("setmaxnreg.inc.sync.aligned.u32 88;\n");
+            if (role != kRoleIdle) run_roles(std::true_type{});
+        }
+    } else if constexpr (M == kPairMode && NKR == 3) {
+        // Register split between warpgroups (pair mode, 7 pairs, 16 warps): warpgroups
+        // 0-1 (gen, combine) give up registers, 2-3 (loader + 7 pair warps) take them,
+        // so the pair warps' row pass can keep loads in flight next to the 2r live
+        // column partial sums. 8 x 96 + 8 x 160 = 16 x 128.
         if (blockDim.x == 512 && np == 7) {
             if (threadIdx.x < 256) {
                 asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(FBF_REGSPLIT_LO));
@@ -1155,14 +1172,14 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                 asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(FBF_REGSPLIT_HI));
                 run_roles(std::true_type{});
             }
-            goto roles_done;
+        } else if (role != kRoleIdle) {
+            run_roles(std::true_type{});
         }
+    } else
+#endif
+    {
+        if (role != kRoleIdle) run_roles(std::true_type{});
     }
-#endif
-    if (role != kRoleIdle) run_roles(std::true_type{});
-#ifndef FBF_NO_REGSPLIT
-roles_done:
-#endif
     if (role == kRoleComb && p.fallbacks) {
         const unsigned w = __reduce_add_sync(0xffffffffu, n_fallbacks);
         if (lane == 0 && w) atomicAdd(p.fallbacks, (unsigned long long)w);
