@@ -59,6 +59,21 @@ def _run(cmd: list[str], log: str) -> None:
         raise RuntimeError(f"build failed: {' '.join(cmd)}\n{p.stdout}{p.stderr}")
 
 
+def _check_inlined(tasks) -> None:
+    """The fused kernel's role lambdas must inline into the kernel: when code growth
+    pushes one out of line, ptxas compiles it as a separate ABI function (its own
+    'Function properties for _ZZN7fbf_dev16fbf_fused_kernel...' entry) with spilled
+    loop state, and the kernel runs ~2x slower (seen on c1: 0.57 -> 0.31 of peak)."""
+    bad = []
+    for _, log in tasks:
+        with open(log) as f:
+            for line in f:
+                if "Function properties for _ZZN7fbf_dev16fbf_fused_kernel" in line:
+                    bad.append(line.split("for ", 1)[1].strip())
+    if bad:
+        raise RuntimeError("fused kernel role code compiled out of line (not inlined): " + ", ".join(bad[:4]))
+
+
 def build(force: bool = False, jobs: int | None = None, verbose: bool = False, out: str | None = None,
           defines: list[str] | None = None, radius: int | None = None) -> str:
     """Builds libfbf.so. Dev options: `out` (another library path), `defines`
@@ -97,6 +112,7 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, o
         futs = [ex.submit(_run, cmd, log) for cmd, log in tasks]
         for f in futs:
             f.result()
+    _check_inlined(tasks)
     tmp = lib + ".tmp"
     _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lpthread"],
          os.path.join(build_dir, "link.log"))
