@@ -98,6 +98,13 @@ __host__ __device__ constexpr bool is_half(int mode) { return mode == kHalfMode 
 #define FBF_REGSPLIT_HI 160
 #endif
 static_assert(FBF_REGSPLIT_LO + FBF_REGSPLIT_HI == 256, "8 warps at LO + 8 at HI must equal 16 warps at 128");
+// kHalfWgMode (5 pairs, 24 warps at 80): gen + combine warpgroups at FBF_WG_LO, the rest at FBF_WG_HI
+#ifndef FBF_WG_LO
+#define FBF_WG_LO 64
+#endif
+#ifndef FBF_WG_HI
+#define FBF_WG_HI 88
+#endif
 constexpr int kHalfMaxPairs = 7;
 // threads of a launch: FFMA2 warps, plus combine, gen and loader (half mode:
 // rounded up to whole sub-partition rows, unused slots idle)
@@ -1152,11 +1159,12 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
         // state around every step. 8 x 64 + 16 x 88 = 24 x 80. Its own instantiation:
         // a second, unsplit copy of the roles in the same function made ptxas spill
         // the COL loops of both copies.
+        static_assert(FBF_WG_LO + 2 * FBF_WG_HI == 3 * 80, "8 warps at LO + 16 at HI must equal 24 warps at 80");
         if (threadIdx.x < 256) {
-            asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n");
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(FBF_WG_LO));
             if (role != kRoleIdle) run_roles(std::false_type{});
         } else {
-            asm volatile("setmaxnreg.inc.sync.aligned.u32 88;\n");
+            asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(FBF_WG_HI));
             if (role != kRoleIdle) run_roles(std::true_type{});
         }
     } else if constexpr (M == kPairMode && NKR == 3) {
