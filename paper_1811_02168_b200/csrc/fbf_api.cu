@@ -403,12 +403,13 @@ bool half_mode_placement(int np, fbf_dev::Params& p) {
     // FFMA2 weight per sub-partition (warp id mod 4; ROW 2, COL half 1): 5 5 5 5.
     static const bool no_split = std::getenv("FBF_HALF_SPLIT") && std::atoi(std::getenv("FBF_HALF_SPLIT")) == 0;
     if (np == 5 && W == 24 && !no_split) {
-        static const unsigned char role[24] = {kRoleGen, kRoleGen, kRoleGen, kRoleGen,      // WG0
-                                               kRoleComb, kRoleComb, kRoleComb, kRoleComb,  // WG1
-                                               kRoleLoad, kRoleCol, kRoleCol, kRoleCol,     // WG2
-                                               kRoleCol, kRoleCol, kRoleCol, kRoleCol,      // WG3
-                                               kRoleRow, kRoleCol, kRoleCol, kRoleCol,      // WG4
-                                               kRoleRow, kRoleRow, kRoleRow, kRoleRow};     // WG5
+        constexpr unsigned char G = kRoleGen, M = kRoleComb, L = kRoleLoad, C = kRoleCol, R = kRoleRow;
+        static const unsigned char layouts[3][24] = {
+            {G, G, G, G, M, M, M, M, L, C, C, C, C, C, C, C, R, C, C, C, R, R, R, R},   // ROW warps highest
+            {G, G, G, G, M, M, M, M, R, R, R, R, R, C, C, C, C, C, C, C, L, C, C, C},   // ROW warps lowest
+            {G, G, G, G, M, M, M, M, L, C, C, C, R, R, R, R, C, C, C, C, R, C, C, C}};  // mixed
+        static const int which = std::getenv("FBF_WG_PERM") ? std::atoi(std::getenv("FBF_WG_PERM")) % 3 : 0;
+        const unsigned char* role = layouts[which];
         int next[6] = {0, 0, 0, 0, 0, 0};
         for (int w = 0; w < 32; ++w) {
             p.warp_role[w] = w < 24 ? role[w] : (unsigned char)kRoleIdle;
