@@ -570,10 +570,14 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
     const int gen_threads = kGenThreads + nrole;   // GEN -> ROW/PAIR and back
     const int col_threads = (is_half(M) ? 2 : 1) * nrole + kCombThreads;  // COL/PAIR -> COMB and back
     constexpr int kFsThreads = kGenThreads + 32;   // GEN -> LOAD (f stage empty)
-    // half-mode rings (two blocks) hand over through named barriers (ROW + COL threads
-    // of all pairs). Split mode keeps the per-pair mbarriers: its 9-pair launches (c3)
-    // measured 0.493 -> 0.489 with the CTA-wide barrier (the pairs lockstep).
-    constexpr bool RING_NB = is_half(M) && RBP == 2;
+    // Ring handoffs through named barriers (ROW + COL threads of all pairs), one id per
+    // step parity and direction: half mode and the split-mode gather ring (r > 16).
+    // ROW at step g waits for COL done with step g - 2 (the block it overwrites was last
+    // read then: RBP - RB + 1 = 2), every step from g = 2 on so the phases pair up.
+    // The split-mode scatter ring (c3) keeps the per-pair mbarriers: its 9-pair
+    // launches measured 0.493 -> 0.489 with the CTA-wide barrier (the pairs lockstep).
+    constexpr bool RING_NB = is_half(M) || (M == kSplitMode && !G::SCATTER);
+    static_assert(!RING_NB || RBP - RB + 1 == 2 || RBP == 2, "ROW may run two steps ahead of COL");
     static_assert(kBarFsEmpty + NFS <= kBarRingFull, "named barrier ids overlap");
     const int ring_threads = (is_half(M) ? 3 : 2) * nrole;
 #ifdef FBF_PHASES
@@ -1061,15 +1065,16 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                     const int gb = (g & (ngb - 1)), blk = g % RBP;
                     PSYNC(0, kBarGenFull + gb, gen_threads);
                     // ring block blk last held step g - RBP, read up to column pass g - RBP + RBN - 1
-                    if (g >= RBP) {
-                        if constexpr (RING_NB) PSYNC(1, kBarRingEmpty + blk, ring_threads);
-                        else PWAIT(1, &ring_empty[pr * RBP + blk], (unsigned)((g / RBP - 1) & 1));
+                    if constexpr (RING_NB) {
+                        if (g >= 2) PSYNC(1, kBarRingEmpty + (g & 1), ring_threads);  // COL done with step g - 2
+                    } else if (g >= RBP) {
+                        PWAIT(1, &ring_empty[pr * RBP + blk], (unsigned)((g / RBP - 1) & 1));
                     }
                     const float4* gin = reinterpret_cast<const float4*>(gen + (((size_t)gb * np + pr) * Q + q) * GS + xc * Q);
                     float2* hout = myring + ((size_t)blk * Q + q) * RS + xc * Q;
                     row_pass<R, Q>(gin, hout, p, kBarGenEmpty + gb, gen_threads);
                     __syncwarp();  // ring block complete
-                    if constexpr (RING_NB) named_arrive(kBarRingFull + blk, ring_threads);
+                    if constexpr (RING_NB) named_arrive(kBarRingFull + (g & 1), ring_threads);
                     else if (lane == 0) mbar_arrive(&ring_full[pr * RBP + blk]);
                 }
             }
@@ -1090,14 +1095,14 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                 for (int t = 0; t < steps; ++t) {
                     const int g = gstep + t;
                     const int blk = g % RBP, cb = (g & (ncb - 1));
-                    if constexpr (RING_NB) PSYNC(0, kBarRingFull + blk, ring_threads);  // always: two blocks
+                    if constexpr (RING_NB) PSYNC(0, kBarRingFull + (g & 1), ring_threads);
                     else PWAIT(0, &ring_full[pr * RBP + blk], (unsigned)((g / RBP) & 1));
                     if (g >= ncb) PSYNC(1, kBarColEmpty + cb, col_threads);
                     float* oc = reinterpret_cast<float*>(colout + ((size_t)cb * np + pr) * Q * kTW) + lane;
                     const float2* hin = hring + (size_t)blk * Q * RS + lane;
                     if (h == 0) col_scatter_half<R, Q, 0>(hin, st, oc, t >= s0, p);
                     else col_scatter_half<R, Q, 1>(hin, st, oc, t >= s0, p);
-                    if constexpr (RING_NB) named_arrive(kBarRingEmpty + blk, ring_threads);  // block free for row pass g + RBP
+                    if constexpr (RING_NB) named_arrive(kBarRingEmpty + (g & 1), ring_threads);  // COL done with step g
                     else if (__syncwarp(), lane == 0) mbar_arrive(&ring_empty[pr * RBP + blk]);
                     named_arrive(kBarColFull + cb, col_threads);
                 }
@@ -1108,14 +1113,14 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                 for (int t = 0; t < steps; ++t) {
                     const int g = gstep + t;
                     const int blk = g % RBP, cb = (g & (ncb - 1));
-                    if constexpr (RING_NB) PSYNC(0, kBarRingFull + blk, ring_threads);  // always: two blocks
+                    if constexpr (RING_NB) PSYNC(0, kBarRingFull + (g & 1), ring_threads);
                     else PWAIT(0, &ring_full[pr * RBP + blk], (unsigned)((g / RBP) & 1));
                     // column buffer cb must have been consumed by COMB even on warm-up steps:
                     // the arrival below completes a phase of col_full[cb]
                     if (g >= ncb) PSYNC(1, kBarColEmpty + cb, col_threads);
                     col_scatter<R, Q>(myring + (size_t)blk * Q * RS + lane, st,
                                       reinterpret_cast<float*>(colout + ((size_t)cb * np + pr) * Q * kTW) + lane, t >= s0, p);
-                    if constexpr (RING_NB) named_arrive(kBarRingEmpty + blk, ring_threads);  // block free for row pass g + RBP
+                    if constexpr (RING_NB) named_arrive(kBarRingEmpty + (g & 1), ring_threads);  // COL done with step g
                     else if (__syncwarp(), lane == 0) mbar_arrive(&ring_empty[pr * RBP + blk]);
                     named_arrive(kBarColFull + cb, col_threads);
                 }
@@ -1124,12 +1129,13 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                     const int g = gstep + t;
                     const int blk = g % RBP, cb = (g & (ncb - 1));
                     const bool do_col = t >= s0;
-                    PWAIT(0, &ring_full[pr * RBP + blk], (unsigned)((g / RBP) & 1));
+                    if constexpr (RING_NB) PSYNC(0, kBarRingFull + (g & 1), ring_threads);
+                    else PWAIT(0, &ring_full[pr * RBP + blk], (unsigned)((g / RBP) & 1));
                     float2 acc[Q];
                     if (do_col) col_pass<R, Q>(myring, blk, lane, p, acc);
-                    __syncwarp();
                     // the oldest block of the window (step g - RB + 1) is free for row pass g - RB + 1 + RBP
-                    if (lane == 0 && g >= RB - 1) mbar_arrive(&ring_empty[pr * RBP + (g - RB + 1) % RBP]);
+                    if constexpr (RING_NB) named_arrive(kBarRingEmpty + (g & 1), ring_threads);  // COL done with step g
+                    else if (__syncwarp(), lane == 0 && g >= RB - 1) mbar_arrive(&ring_empty[pr * RBP + (g - RB + 1) % RBP]);
                     // column buffer cb must have been consumed by COMB even on warm-up steps:
                     // the arrival below completes a phase of col_full[cb]
                     if (g >= ncb) PSYNC(1, kBarColEmpty + cb, col_threads);
