@@ -43,6 +43,7 @@ using LaunchFn = cudaError_t (*)(const Params&, const CUtensorMap&, int, cudaStr
 struct QEntry {
     LaunchFn launch[kMaxKR + 1] = {};
     int max_pairs[3][3] = {};  // [ngb][ncb], 1..2
+    int duo_max_pairs[3][3] = {};  // the same with the duo exchange region appended
 };
 struct RadiusEntry {
     QEntry split8;          // split mode, Q = 8 (every radius)
@@ -61,9 +62,13 @@ QEntry qentry() {
     e.launch[3] = &launch_fused<R, Q, 3, M>;
     if constexpr (!is_half(M)) e.launch[4] = &launch_fused<R, Q, 4, M>;
     for (int ngb = 1; ngb <= 2; ++ngb)
-        for (int ncb = 1; ncb <= 2; ++ncb)
+        for (int ncb = 1; ncb <= 2; ++ncb) {
             e.max_pairs[ngb][ncb] = is_half(M) ? std::min(kHalfMaxPairs, G::max_pairs(ngb, ncb))
                                                    : G::max_pairs(ngb, ncb);
+            int d = e.max_pairs[ngb][ncb];
+            while (d > 0 && align128(G::smem_bytes(d, ngb, ncb)) + duo_xchg_bytes(Q) > kSmemLimit) --d;
+            e.duo_max_pairs[ngb][ncb] = d;
+        }
     return e;
 }
 
@@ -580,6 +585,36 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
         return v ? std::atoi(v) : -1;
     }();
     p.pdl = pdl_env >= 0 ? pdl_env : (p.total_units < 1024LL * grid ? 1 : 0);
+    p.inv_period = a.turns();
+
+    // Duo launch for two-chunk plans (c2: K = 9, 9 + 8 pairs): clusters of 2 CTAs, each
+    // work share filtered by both ranks at once, rank 1's (num, den) partials handed to
+    // rank 0 per step through distributed shared memory -- one launch, no HBM scratch,
+    // the same bits as the two scratch launches. FBF_DUO=0 (dev) keeps the scratch path.
+    static const bool duo_off = std::getenv("FBF_DUO") && std::atoi(std::getenv("FBF_DUO")) == 0;
+    auto nkr_of = [](const Chunk& c) { return c.n_k - (c.k_lo == 0 ? 1 : 0); };
+    if (!duo_off && plan.chunks.size() == 2 && plan.mode != fbf_dev::kHalfMode && ctx.num_sms >= 2 &&
+        nkr_of(plan.chunks[0]) == nkr_of(plan.chunks[1]) &&
+        std::max(plan.chunks[0].n_pairs, plan.chunks[1].n_pairs) <= plan.ent->duo_max_pairs[plan.ngb][plan.ncb]) {
+        const int clusters = (int)std::max(1LL, std::min<long long>((long long)ctx.num_sms / 2, (want + 1) / 2));
+        p.duo = 1;
+        p.pdl = 0;
+        p.acc = nullptr;
+        p.col_rounds = contig ? 0 : (int)(((long long)job.n_frames * p.n_strips) / clusters);
+        for (int rk = 0; rk < 2; ++rk) {
+            const Chunk& c = plan.chunks[rk == 0 ? 1 : 0];  // rank 0: the last chunk (writes the output)
+            auto& d = p.duo_chunk[rk];
+            d.k_lo = c.k_lo;
+            d.n_pairs = c.n_pairs;
+            d.k_first = std::max(c.k_lo, 1);
+            for (int kk = 0; kk < c.n_k; ++kk) d.coeff[kk] = (float)a.c[c.k_lo + kk];
+        }
+        p.n_pairs = std::max(plan.chunks[0].n_pairs, plan.chunks[1].n_pairs);
+        const cudaError_t e = plan.ent->launch[nkr_of(plan.chunks[0])](p, tmap, 2 * clusters, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "fbf_fused_kernel duo launch");
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return FBF_OK;
+    }
 
     for (size_t ci = 0; ci < plan.chunks.size(); ++ci) {
         const Chunk& c = plan.chunks[ci];
@@ -590,7 +625,6 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
         p.first_chunk = ci == 0;
         p.last_chunk = ci + 1 == plan.chunks.size();
         for (int kk = 0; kk < c.n_k; ++kk) p.coeff[kk] = (float)a.c[c.k_lo + kk];
-        p.inv_period = a.turns();
         p.k_first = std::max(c.k_lo, 1);
         const bool wg = plan.mode == fbf_dev::kHalfMode && half_mode_placement(c.n_pairs, p);
         const fbf_dev::QEntry* qe = wg ? plan.ent_wg : plan.ent;  // every radius has the split variant

@@ -45,6 +45,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <atomic>
 #include <type_traits>
 
@@ -112,6 +113,10 @@ __host__ __device__ constexpr int block_threads(int pairs, int mode) {
     return is_half(mode) ? 4 * ((3 * pairs + kGenWarps + kCombWarps + 1 + 3) / 4) * 32
                              : (mode == kPairMode ? 1 : 2) * 32 * pairs + kExtraThreads;
 }
+// Duo exchange region (appended to the larger rank's layout): [2 slots][Q * kTW / 2
+// pixel pairs] float4 (num a, num b, den a, den b), then the slot barriers full[2], empty[2].
+__host__ __device__ constexpr size_t duo_xchg_bytes(int q) { return 2 * (size_t)q * (kTW / 2) * 16 + 4 * 8; }
+__host__ __device__ constexpr size_t align128(size_t v) { return (v + 127) / 128 * 128; }
 enum Role { kRoleGen = 0, kRoleRow = 1, kRoleCol = 2, kRoleLoad = 3, kRoleComb = 4, kRoleIdle = 5 };
 
 
@@ -152,6 +157,16 @@ struct Params {
     int use_tma2d;               // interior f tiles by the tensor map (kernel parameter `tmap`)
     int col_rounds;              // whole columns (frame, strip) per CTA taken round-robin before the tail
     int pdl;                     // host: launch with programmatic stream serialization
+    // Duo launch (two coefficient chunks, no HBM scratch): clusters of 2 CTAs share each
+    // work unit; rank r runs duo_chunk[r]. Rank 1 (the first chunk, k from 0) hands its
+    // (num, den) partial sums per step to rank 0 (the last chunk) through distributed
+    // shared memory; rank 0 continues from them exactly as the second launch of the
+    // scratch path continues from the scratch image (same bits).
+    int duo;
+    struct ChunkSel {
+        int k_lo, n_pairs, k_first;
+        float coeff[kMaxKR + 1];
+    } duo_chunk[2];
 };
 
 #ifdef FBF_PHASES
@@ -203,10 +218,10 @@ struct Geometry {
     static constexpr size_t bar_bytes = 8 * n_bars + 8;          // mbarriers + counter
     static constexpr size_t misc_bytes = (bar_bytes + 127) / 128 * 128;
     static constexpr size_t fixed_bytes = fstage_bytes + misc_bytes;
-    static constexpr size_t pair_bytes(int ngb, int ncb) {
+    __host__ __device__ static constexpr size_t pair_bytes(int ngb, int ncb) {
         return sizeof(float2) * (size_t)(ngb * Q * GS + ncb * Q * kTW + RROWS * RS);
     }
-    static constexpr size_t smem_bytes(int pairs, int ngb, int ncb) { return fixed_bytes + pair_bytes(ngb, ncb) * pairs; }
+    __host__ __device__ static constexpr size_t smem_bytes(int pairs, int ngb, int ncb) { return fixed_bytes + pair_bytes(ngb, ncb) * pairs; }
     static int max_pairs(int ngb, int ncb) {
         size_t budget = kSmemPerSM - kSmemReservedPerBlock;
         if (budget > kSmemLimit) budget = kSmemLimit;
@@ -336,6 +351,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "r"(parity), "r"(1000000u)
         : "memory");
 }
+// Duo exchange: wait on a local mbarrier whose arrivals come from the peer CTA
+// (acquire at cluster scope, so the peer's distributed-shared-memory stores are visible)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAITC_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra WAITC_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
+// arrive (release at cluster scope) on an mbarrier in the peer CTA's shared memory
+__device__ __forceinline__ void mbar_arrive_remote(unsigned cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+
 // Named CTA barriers for the warp-role handoffs: producers bar.arrive (no
 // wait), consumers bar.sync -- a consumer warp blocked in bar.sync issues
 // nothing, where an mbarrier try_wait loop keeps waking up (measured: the
@@ -524,7 +557,20 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
     constexpr int GW = G::GW, GS = G::GS, FSW = G::FSW, RB = G::RB, RBP = G::RBP, RROWS = G::RROWS, RS = G::RS;
     constexpr int NFS = G::NFS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int np = p.n_pairs, ngb = p.ngb, ncb = p.ncb;  // ngb, ncb in {1, 2}: buffer index = g & (n - 1)
+    const bool duo = p.duo != 0;
+    unsigned crank = 0;  // rank in the cluster (duo launches)
+    if (duo) asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(crank));
+    // this CTA's coefficient chunk
+    const int np = duo ? p.duo_chunk[crank].n_pairs : p.n_pairs;
+    const int k_lo = duo ? p.duo_chunk[crank].k_lo : p.k_lo;
+    const int k_first = duo ? p.duo_chunk[crank].k_first : p.k_first;
+    const float* coeff = duo ? p.duo_chunk[crank].coeff : p.coeff;
+    // (num, den) carried between chunks: into the combine (scratch image or, duo rank 0,
+    // the exchange slots), out of it (scratch or, duo rank 1, the peer's exchange slots)
+    const bool x_in = duo && crank == 0, x_out = duo && crank == 1;
+    const bool carry_in = duo ? x_in : !p.first_chunk;
+    const bool last = duo ? x_in : p.last_chunk != 0;
+    const int ngb = p.ngb, ncb = p.ncb;  // ngb, ncb in {1, 2}: buffer index = g & (n - 1)
     float* fstage = reinterpret_cast<float*>(smem_raw);                         // [NFS][Q][FSW]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + G::fstage_bytes);
     uint64_t* fs_full = bars;                                // [NFS] LOAD -> GEN (cp.async completion)
@@ -533,6 +579,10 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
     float2* gen = reinterpret_cast<float2*>(smem_raw + G::fixed_bytes);  // [ngb][np][Q][GS]
     float2* colout = gen + (size_t)ngb * np * Q * GS;                    // [ncb][np] x [2][Q][TW] floats
     float2* ring = colout + (size_t)ncb * np * Q * kTW;                  // [np][RROWS][RS]
+    // duo exchange region, after the larger rank's layout (the same offset in both CTAs)
+    const size_t xoff = duo ? align128(G::smem_bytes(max(p.duo_chunk[0].n_pairs, p.duo_chunk[1].n_pairs), p.ngb, p.ncb)) : 0;
+    float4* xslot = reinterpret_cast<float4*>(smem_raw + xoff);              // [2][Q * kTW / 2]
+    uint64_t* xbar = reinterpret_cast<uint64_t*>(smem_raw + xoff + 2 * (size_t)Q * (kTW / 2) * 16);  // full[2], empty[2]
 
     const int nrole = np * 32;  // threads of the ROW/PAIR role (and of the COL role in split mode)
     const int nf = G::PAIR ? nrole : 2 * nrole;  // FFMA2 threads
@@ -551,7 +601,8 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
         else if (t < nf)                   { role = kRoleCol; tid = t - nrole; }
         else if (t < nf + kCombThreads)    { role = kRoleComb; tid = t - nf; }
         else if (t < nf + CG)              { role = kRoleGen; tid = t - nf - kCombThreads; }
-        else                               { role = kRoleLoad; tid = t - nf - CG; }
+        else if (t < nf + CG + 32)         { role = kRoleLoad; tid = t - nf - CG; }
+        else                               { role = kRoleIdle; tid = 0; }  // duo rank with fewer pairs
 #ifndef FBF_NO_REGSPLIT
         // register-split layout (pair mode, 7 pairs, 16 warps): warpgroups 2-3 hold the
         // 7 pair warps and the loader, 0-1 the combine and gen warps, so that every
@@ -565,7 +616,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
 #endif
     }
     const int lane = threadIdx.x & 31;
-    const int zk = p.k_lo == 0 ? 1 : 0;  // k = 0 contributes the single pair (f, 1)
+    const int zk = k_lo == 0 ? 1 : 0;  // k = 0 contributes the single pair (f, 1)
     // named-barrier thread counts: producers + consumers of each handoff
     const int gen_threads = kGenThreads + nrole;   // GEN -> ROW/PAIR and back
     const int col_threads = (is_half(M) ? 2 : 1) * nrole + kCombThreads;  // COL/PAIR -> COMB and back
@@ -585,15 +636,23 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
     const long long _pt0 = clock64();
 #endif
     unsigned n_fallbacks = 0;  // combine threads: fallback pixels (filter.cpp:203-208)
+    unsigned xstep = 0;        // combine threads, duo: output steps exchanged so far
     if (threadIdx.x == 0) {
         for (int b = 0; b < NFS; ++b) mbar_init(&fs_full[b], 1);
         for (int b = 0; b < np * RBP; ++b) {
             mbar_init(&ring_full[b], 1);
             mbar_init(&ring_empty[b], is_half(M) ? 2 : 1);  // both COL halves release a block
         }
+        if (duo) {
+            for (int b = 0; b < 4; ++b) mbar_init(&xbar[b], kCombThreads);  // full[2], empty[2]
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    __syncthreads();
+    if (duo) {  // the peer's exchange barriers are initialised before any remote arrive
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    } else {
+        __syncthreads();
+    }
     // Programmatic dependent launch: this grid may start while the previous kernel on
     // the stream drains (its CTAs free SMs at different times). Wait for that grid and
     // its memory (the previous chunk's (num, den) scratch, a caller's producer kernel)
@@ -608,9 +667,11 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
     // are read from DRAM once (L2 hits for the second) -- then a contiguous share of
     // the remaining (frame, strip, row) units.
     const long long U = p.total_units;
-    const long long tail0 = (long long)p.col_rounds * gridDim.x * p.out_rows;  // first unit of the tail
-    const long long u_begin = tail0 + (U - tail0) * blockIdx.x / gridDim.x;
-    const long long u_end = tail0 + (U - tail0) * (blockIdx.x + 1) / gridDim.x;
+    // work shares: one per CTA, or per cluster of 2 in a duo launch (both ranks walk it)
+    const int wid = duo ? (int)(blockIdx.x >> 1) : (int)blockIdx.x, nw = duo ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    const long long tail0 = (long long)p.col_rounds * nw * p.out_rows;  // first unit of the tail
+    const long long u_begin = tail0 + (U - tail0) * wid / nw;
+    const long long u_end = tail0 + (U - tail0) * (wid + 1) / nw;
     const long long per_frame = (long long)p.n_strips * p.out_rows;
     // steps start e rows early so that output rows begin exactly at ya; the first
     // s0 steps of a segment only fill the ring
@@ -667,7 +728,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
         }
         const unsigned nrows = (unsigned)max(hi - lo, 0);
         const float inv = p.inv_period;
-        const bool kfirst = p.k_first > 1;
+        const bool kfirst = k_first > 1;
         // MASKED: zero border -- pixels outside the image and rows outside the needed
         // window contribute exact zeros. Symmetric / replicate borders map every staged
         // pixel into the image, and rows outside [lo, hi) (stale stage data) only reach
@@ -697,8 +758,8 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                     if (NKR > 0) {
                         const CS2 h = harmonic1x2(f, inv);
                         const float2 w0 = make_float2(h.c.x, h.s.x), w1 = make_float2(h.c.y, h.s.y);
-                        float2 z0 = kfirst ? harmonic_first1(w0, p.k_first) : w0;
-                        float2 z1 = kfirst ? harmonic_first1(w1, p.k_first) : w1;
+                        float2 z0 = kfirst ? harmonic_first1(w0, k_first) : w0;
+                        float2 z1 = kfirst ? harmonic_first1(w1, k_first) : w1;
                         if constexpr (MASKED) {
                             if (!va) z0 = make_float2(0.f, 0.f);
                             if (!vb) z1 = make_float2(0.f, 0.f);
@@ -768,7 +829,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
             nd[it] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (ci[it].y < sg.yb && ci[it].colok) {
                 fv[it] = make_float2(__ldg(ci[it].sp), ci[it].vb ? __ldg(ci[it].sp + 1) : 0.f);
-                if (!p.first_chunk) {
+                if (carry_in && !x_in) {
                     const float2 a = __ldcg(ci[it].ap), b = ci[it].vb ? __ldcg(ci[it].ap + 1) : make_float2(0.f, 0.f);
                     nd[it] = make_float4(a.x, b.x, a.y, b.y);  // (num a, num b, den a, den b)
                 }
@@ -779,9 +840,9 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
     const long long src_step = (long long)Q * p.src_pitch, dst_step = (long long)Q * p.dst_pitch,
                     acc_step = (long long)Q * p.width;
     auto combine_step = [&](const Segment& sg, int cb, CombItem (&ci)[CITER], const float2 (&fv)[CITER],
-                            const float4 (&nd)[CITER]) {
+                            const float4 (&nd)[CITER], unsigned xdst) {
         const float* cbase = reinterpret_cast<const float*>(colout + cb * np * Q * kTW);
-        const bool kfirst_c = p.k_first > 1;
+        const bool kfirst_c = k_first > 1;
 #pragma unroll
         for (int it = 0; it < CITER; ++it) {
             CombItem& c = ci[it];
@@ -792,7 +853,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                 if (p.bad_pixels && !(f.x >= 0.f && f.x <= p.range_max && f.y >= 0.f && f.y <= p.range_max))
                     atomicOr(p.bad_pixels, 1u);
                 float2 num = make_float2(0.f, 0.f), den = make_float2(0.f, 0.f);
-                if (!p.first_chunk) {
+                if (carry_in) {
                     num = make_float2(nd[it].x, nd[it].y);
                     den = make_float2(nd[it].z, nd[it].w);
                 }
@@ -804,17 +865,17 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                 auto accumulate = [&](auto zkc) {
                     constexpr int ZK = decltype(zkc)::value;
                     if (ZK) {
-                        const float2 c0 = make_float2(p.coeff[0], p.coeff[0]);
+                        const float2 c0 = make_float2(coeff[0], coeff[0]);
                         num = __ffma2_rn(c0, go[0], num);
                         den = __ffma2_rn(c0, go[CSTR], den);
                     }
                     if (NKR > 0) {
                         const CS2 c1 = harmonic1x2(f, p.inv_period);
-                        CS2 cs = kfirst_c ? harmonic_first2(c1, p.k_first) : c1;
+                        CS2 cs = kfirst_c ? harmonic_first2(c1, k_first) : c1;
                         const float2* gk = go + ZK * 2 * CSTR;
 #pragma unroll
                         for (int kk = 0; kk < NKR; ++kk) {
-                            const float2 ck = make_float2(p.coeff[ZK + kk], p.coeff[ZK + kk]);
+                            const float2 ck = make_float2(coeff[ZK + kk], coeff[ZK + kk]);
                             const float2* pn = gk + (4 * kk) * CSTR;  // G(C_k f), G(S_k f)
                             const float2* pd = pn + 2 * CSTR;         // G(C_k), G(S_k)
                             num = __ffma2_rn(ck, __ffma2_rn(cs.s, pn[CSTR], __fmul2_rn(cs.c, pn[0])), num);
@@ -825,7 +886,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                 };
                 if (zk) accumulate(std::integral_constant<int, 1>{});
                 else accumulate(std::integral_constant<int, 0>{});
-                if (p.last_chunk) {
+                if (last) {
                     float oa = f.x, ob = f.y;
                     unsigned nfb = 0;
                     if (den.x > 1e-12f) oa = num.x * rcp_approx(den.x); else ++nfb;
@@ -833,6 +894,11 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                     n_fallbacks += nfb;
                     c.dp[0] = oa;
                     if (vb) c.dp[1] = ob;
+                } else if (x_out) {  // into the peer's exchange slot (distributed shared memory)
+                    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(
+                                     xdst + (unsigned)(it * kCombThreads + tid) * 16u),
+                                 "f"(num.x), "f"(num.y), "f"(den.x), "f"(den.y)
+                                 : "memory");
                 } else {
                     c.ap[0] = make_float2(num.x, den.x);
                     if (vb) c.ap[1] = make_float2(num.y, den.y);
@@ -841,7 +907,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
             c.y += Q;
             c.sp += src_step;
             c.dp += dst_step;
-            if (!p.first_chunk || !p.last_chunk) c.ap += acc_step;
+            if (p.acc) c.ap += acc_step;
         }
     };
 
@@ -855,7 +921,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
             // one call site of `body` (two loops would inline every role twice)
             long long next, a, b;
             if (j < p.col_rounds) {
-                a = ((long long)j++ * gridDim.x + blockIdx.x) * p.out_rows;
+                a = ((long long)j++ * nw + wid) * p.out_rows;
                 b = a + p.out_rows;
             } else if (u < u_end) {
                 a = u;
@@ -999,6 +1065,16 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
             }
         });
     } else if (role == kRoleComb) {
+        // duo: exchange slot s = xstep & 1 of the xstep-th output step; rank 1 writes the peer's
+        // slot after the peer freed it (empty[s], arrived remotely), then arrives on the
+        // peer's full[s]; rank 0 waits full[s], reads, and arrives on rank 1's empty[s]
+        unsigned xpeer_slot = 0, xpeer_bar = 0;
+        if (duo) {
+            const unsigned peer = crank ^ 1u;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(xpeer_slot) : "r"(smem_u32(xslot)), "r"(peer));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(xpeer_bar) : "r"(smem_u32(xbar)), "r"(peer));
+        }
+        constexpr unsigned XI = Q * (kTW / 2);  // pixel pairs per output step
         for_each_segment([&](const Segment& sg, const int gstep) {
         FBF_SEGMENT_LOCALS
             // ============================ COMB ==============================
@@ -1009,14 +1085,28 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                 const int cb = (g & (ncb - 1));
                 float2 fv[CITER];
                 float4 nd[CITER];
-                if (t >= s0) combine_load(sg, ci, fv, nd);
+                const unsigned slot = xstep & 1u, xpar = (xstep >> 1) & 1u;
+                if (t >= s0) {
+                    combine_load(sg, ci, fv, nd);
+                    if (x_in) {  // the peer's (num, den) for these pixels
+                        mbar_wait_cluster(&xbar[slot], xpar);
+#pragma unroll
+                        for (int it = 0; it < CITER; ++it) nd[it] = xslot[slot * XI + it * kCombThreads + tid];
+                    }
+                    if (x_out && xstep >= 2) mbar_wait_cluster(&xbar[2 + slot], xpar ^ 1u);  // the peer read slot
+                }
                 PSYNC(0, kBarColFull + cb, col_threads);
 #ifndef FBF_SKIP_COMB
 #ifdef FBF_DEV_LIGHT_W0
                 if (tid < 32)
 #endif
-                if (t >= s0) combine_step(sg, cb, ci, fv, nd);
+                if (t >= s0) combine_step(sg, cb, ci, fv, nd, xpeer_slot + slot * XI * 16u);
 #endif
+                if (duo && t >= s0) {
+                    // rank 1: slot written -> peer's full[slot]; rank 0: slot read -> peer's empty[slot]
+                    mbar_arrive_remote(xpeer_bar + 8u * (x_out ? slot : 2u + slot));
+                    ++xstep;
+                }
                 named_arrive(kBarColEmpty + cb, col_threads);  // this warp is done with column buffer cb
             }
         });
@@ -1198,6 +1288,9 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
         const unsigned w = __reduce_add_sync(0xffffffffu, n_fallbacks);
         if (lane == 0 && w) atomicAdd(p.fallbacks, (unsigned long long)w);
     }
+    // duo: neither CTA exits while its peer may still write its exchange slots or
+    // arrive on its barriers
+    if (duo) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 #ifdef FBF_PHASES
     if (p.prof && lane == 0) {
         unsigned long long* pw = p.prof + 4 * (threadIdx.x / 32);
@@ -1212,7 +1305,10 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
 template <int R, int Q, int NKR, int M>
 cudaError_t launch_fused(const Params& p, const CUtensorMap& tmap, int grid, cudaStream_t stream) {
     using G = Geometry<R, Q, M>;
-    const size_t smem = G::smem_bytes(p.n_pairs, p.ngb, p.ncb);
+    // duo: both CTAs allocate the larger rank's layout plus the exchange region
+    const int np_max = p.duo ? std::max(p.duo_chunk[0].n_pairs, p.duo_chunk[1].n_pairs) : p.n_pairs;
+    const size_t smem = p.duo ? align128(G::smem_bytes(np_max, p.ngb, p.ncb)) + duo_xchg_bytes(Q)
+                              : G::smem_bytes(p.n_pairs, p.ngb, p.ncb);
     // The dynamic shared-memory opt-in is a property of the function in the
     // CURRENT device's context: set it once per device (bit d of the mask), safe
     // against concurrent launches from the per-device host threads (a second
@@ -1234,14 +1330,20 @@ cudaError_t launch_fused(const Params& p, const CUtensorMap& tmap, int grid, cud
     const bool pdl = p.pdl != 0;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3((unsigned)block_threads(p.n_pairs, M));
+    cfg.blockDim = dim3((unsigned)block_threads(np_max, M));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    if (p.duo) {  // clusters of 2 CTAs (instead of PDL)
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = (pdl || p.duo) ? 1 : 0;
     e = cudaLaunchKernelEx(&cfg, fbf_fused_kernel<R, Q, NKR, M>, p, tmap);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
