@@ -19,6 +19,8 @@ CASES = [
     (100, 90, 16.0 / 3.0, 40.0, 0.05, "symmetric"),
     (150, 120, 8.0, 15.0, 0.01, "replicate"),
     (97, 333, 10.0, 80.0, 0.05, "symmetric"),
+    (120, 100, 8.0, 15.0, 0.01, "zero"),       # r = 24, K = 9: two chunks (duo / scratch)
+    (700, 64, 10.0, 80.0, 0.05, "zero"),       # r = 30, K = 3: the c4 kernel (warpgroup split)
 ]
 
 

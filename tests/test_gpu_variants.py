@@ -2,8 +2,10 @@
 
 The planner (fbf_api.cu make_plan) picks, per launch, the step height Q (8/16),
 the warp organisation (pair mode: one warp per channel pair with the scatter
-column pass; split mode: row and column warps with a ring) and the buffer
-depths. All variants run the same per-pixel arithmetic in the same order, so
+column pass; split mode: row and column warps with a ring; half mode) and the
+buffer depths; the host picks the f-tile staging, the work order, programmatic
+dependent launch and, for two coefficient chunks, one duo launch or two launches
+with an HBM scratch. All variants run the same per-pixel arithmetic in the same order, so
 their outputs must be bit-identical; the default plan is checked against the
 oracle in test_gpu_parity.py, the variants here against it and the oracle."""
 import os
@@ -28,6 +30,15 @@ VARIANTS = {
     "half_q8": {"FBF_MODE": "2", "FBF_Q": "8"},
     "half_q8_single_buffers": {"FBF_MODE": "2", "FBF_Q": "8", "FBF_NGB": "1", "FBF_NCB": "1"},
     "bulk_staging": {"FBF_STAGE": "bulk"},
+    "element_staging": {"FBF_STAGE": "elem"},
+    # two-chunk plans as two launches with the HBM (num, den) scratch instead of one duo
+    # (2-CTA cluster) launch; the duo rank 0 continues from rank 1's partials exactly as
+    # the second launch continues from the scratch
+    "scratch_chunks": {"FBF_DUO": "0"},
+    "contiguous_work_order": {"FBF_ORDER": "contig"},
+    "pdl_off": {"FBF_PDL": "0"},
+    "pdl_on": {"FBF_PDL": "1"},
+    "half_without_warpgroup_split": {"FBF_HALF_SPLIT": "0"},
 }
 
 
@@ -38,7 +49,8 @@ def variant_outputs(gpu, tmp_path_factory):
     for name, env in VARIANTS.items():
         path = str(d / f"{name}.npz")
         e = dict(os.environ)
-        for k in ("FBF_MODE", "FBF_Q", "FBF_NGB", "FBF_NCB", "FBF_STAGE"):
+        for k in ("FBF_MODE", "FBF_Q", "FBF_NGB", "FBF_NCB", "FBF_STAGE", "FBF_DUO", "FBF_ORDER", "FBF_PDL",
+                  "FBF_HALF_SPLIT", "FBF_WGQ"):
             e.pop(k, None)
         e.update(env)
         subprocess.run([sys.executable, os.path.join(ROOT, "tests", "_variant_run.py"), path], env=e, check=True,
