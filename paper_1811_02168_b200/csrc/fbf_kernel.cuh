@@ -1120,6 +1120,11 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                 const int pr = tid / 32;
                 const int q = lane % Q, xc = lane / Q;
                 float2* hbuf = ring + (size_t)pr * RROWS * RS;
+                // per-buffer addresses, selected per step (no per-step address arithmetic)
+                const float4* gin0 = reinterpret_cast<const float4*>(gen + ((size_t)pr * Q + q) * GS + xc * Q);
+                const float4* gin1 = gin0 + (size_t)np * Q * GS / 2;
+                float* oc0 = reinterpret_cast<float*>(colout + (size_t)pr * Q * kTW) + lane;
+                float* oc1 = oc0 + (size_t)np * Q * kTW * 2;
                 float2 st[2 * R];
 #pragma unroll
                 for (int i = 0; i < 2 * R; ++i) st[i] = make_float2(0.f, 0.f);  // new segment
@@ -1127,16 +1132,12 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                     const int g = gstep + t;
                     const int gb = (g & (ngb - 1)), cb = (g & (ncb - 1));
                     PSYNC(0, kBarGenFull + gb, gen_threads);
-                    const float4* gin =
-                        reinterpret_cast<const float4*>(gen + (((size_t)gb * np + pr) * Q + q) * GS + xc * Q);
-                    row_pass<R, Q>(gin, hbuf + (size_t)q * RS + xc * Q, p,
-                                   kBarGenEmpty + gb, gen_threads);
+                    row_pass<R, Q>(gb ? gin1 : gin0, hbuf + (size_t)q * RS + xc * Q, p, kBarGenEmpty + gb, gen_threads);
                     __syncwarp();  // the step's row-pass block is complete
                     // column buffer cb must have been consumed by COMB even on warm-up steps:
                     // the arrival below completes a phase of col_full[cb]
                     if (g >= ncb) PSYNC(1, kBarColEmpty + cb, col_threads);
-                    col_scatter<R, Q>(hbuf + lane, st, reinterpret_cast<float*>(colout + ((size_t)cb * np + pr) * Q * kTW) + lane, t >= s0,
-                                      p);
+                    col_scatter<R, Q>(hbuf + lane, st, cb ? oc1 : oc0, t >= s0, p);
                     named_arrive(kBarColFull + cb, col_threads);
                 }
             }
@@ -1150,6 +1151,9 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                 const int q = lane % Q, xc = lane / Q;
                 static_assert(Q * (kTW / Q) == 32, "one warp covers a step of one pair");
                 float2* myring = ring + (size_t)pr * RROWS * RS;
+                const float4* gin0 = reinterpret_cast<const float4*>(gen + ((size_t)pr * Q + q) * GS + xc * Q);
+                const float4* gin1 = gin0 + (size_t)np * Q * GS / 2;
+                float2* hout0 = myring + (size_t)q * RS + xc * Q;
                 for (int t = 0; t < steps; ++t) {
                     const int g = gstep + t;
                     const int gb = (g & (ngb - 1)), blk = g % RBP;
@@ -1160,9 +1164,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                     } else if (g >= RBP) {
                         PWAIT(1, &ring_empty[pr * RBP + blk], (unsigned)((g / RBP - 1) & 1));
                     }
-                    const float4* gin = reinterpret_cast<const float4*>(gen + (((size_t)gb * np + pr) * Q + q) * GS + xc * Q);
-                    float2* hout = myring + ((size_t)blk * Q + q) * RS + xc * Q;
-                    row_pass<R, Q>(gin, hout, p, kBarGenEmpty + gb, gen_threads);
+                    row_pass<R, Q>(gb ? gin1 : gin0, hout0 + (size_t)blk * Q * RS, p, kBarGenEmpty + gb, gen_threads);
                     __syncwarp();  // ring block complete
                     if constexpr (RING_NB) named_arrive(kBarRingFull + (g & 1), ring_threads);
                     else if (lane == 0) mbar_arrive(&ring_full[pr * RBP + blk]);
@@ -1179,6 +1181,10 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
             } else if constexpr (is_half(M)) {
                 const int pr = tid / 64, h = (tid / 32) & 1;  // pair, output-row parity
                 const float2* hring = ring + (size_t)pr * RROWS * RS;
+                const float2* hin0 = hring + lane;
+                const float2* hin1 = hin0 + (size_t)Q * RS;  // RBP == 2
+                float* oc0 = reinterpret_cast<float*>(colout + (size_t)pr * Q * kTW) + lane;
+                float* oc1 = oc0 + (size_t)np * Q * kTW * 2;
                 float2 st[R];
 #pragma unroll
                 for (int i = 0; i < R; ++i) st[i] = make_float2(0.f, 0.f);  // new segment
@@ -1188,8 +1194,8 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                     if constexpr (RING_NB) PSYNC(0, kBarRingFull + (g & 1), ring_threads);
                     else PWAIT(0, &ring_full[pr * RBP + blk], (unsigned)((g / RBP) & 1));
                     if (g >= ncb) PSYNC(1, kBarColEmpty + cb, col_threads);
-                    float* oc = reinterpret_cast<float*>(colout + ((size_t)cb * np + pr) * Q * kTW) + lane;
-                    const float2* hin = hring + (size_t)blk * Q * RS + lane;
+                    float* oc = cb ? oc1 : oc0;
+                    const float2* hin = blk ? hin1 : hin0;
                     if (h == 0) col_scatter_half<R, Q, 0>(hin, st, oc, t >= s0, p);
                     else col_scatter_half<R, Q, 1>(hin, st, oc, t >= s0, p);
                     if constexpr (RING_NB) named_arrive(kBarRingEmpty + (g & 1), ring_threads);  // COL done with step g
@@ -1197,6 +1203,10 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                     named_arrive(kBarColFull + cb, col_threads);
                 }
             } else if constexpr (G::SCATTER) {
+                const float2* hin0 = myring + lane;
+                const float2* hin1 = hin0 + (size_t)Q * RS;  // RBP == 2
+                float* oc0 = reinterpret_cast<float*>(colout + (size_t)pr * Q * kTW) + lane;
+                float* oc1 = oc0 + (size_t)np * Q * kTW * 2;
                 float2 st[2 * R];
 #pragma unroll
                 for (int i = 0; i < 2 * R; ++i) st[i] = make_float2(0.f, 0.f);  // new segment
@@ -1208,8 +1218,7 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
                     // column buffer cb must have been consumed by COMB even on warm-up steps:
                     // the arrival below completes a phase of col_full[cb]
                     if (g >= ncb) PSYNC(1, kBarColEmpty + cb, col_threads);
-                    col_scatter<R, Q>(myring + (size_t)blk * Q * RS + lane, st,
-                                      reinterpret_cast<float*>(colout + ((size_t)cb * np + pr) * Q * kTW) + lane, t >= s0, p);
+                    col_scatter<R, Q>(blk ? hin1 : hin0, st, cb ? oc1 : oc0, t >= s0, p);
                     if constexpr (RING_NB) named_arrive(kBarRingEmpty + (g & 1), ring_threads);  // COL done with step g
                     else if (__syncwarp(), lane == 0) mbar_arrive(&ring_empty[pr * RBP + blk]);
                     named_arrive(kBarColFull + cb, col_threads);
