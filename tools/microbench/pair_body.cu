@@ -1,3 +1,5 @@
+#include <vector>
+#include <cstdlib>
 // dev tool: FFMA2 efficiency of the pair-warp body (row pass into a ring, column
 // pass out of it) for step heights Q (= outputs per lane P), sequential or
 // interleaved passes, and warps per SM. No inter-warp synchronisation: the
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(384, 1) body(const Taps tp, float* sink, int s
   if (out[lane].x == 12345.f) sink[0] = 1.f;
 }
 
-int main() {
+int main(int argc, char** argv) {
   Taps tp; for (int j = 0; j <= R; j++) tp.t[j] = 1.f / (1 + j);
   float* sink; cudaMalloc(&sink, 4);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -191,7 +193,10 @@ int main() {
     double flops = 148.0 * warps * steps * 2.0 * (q * TW) * (2 * R + 1) * 4;
     printf("%s warps %2d: %.1f%% of 74.45 TF  (%s)\n", name, warps, flops / ms / 1e9 / 74.45 * 100, cudaGetErrorString(cudaGetLastError()));
   };
-  for (int wps : {7}) {
+  // warps per CTA from the command line (default 7): 4 = one FFMA2 warp per sub-partition
+  std::vector<int> wlist; for (int i = 1; i < argc; ++i) wlist.push_back(atoi(argv[i]));
+  if (wlist.empty()) wlist.push_back(7);
+  for (int wps : wlist) {
     run(body<16, 2>, 16, wps, sizeof(float2) * Geo<16>::floats2, "scat  Q=16");
     run(body<16, 2, 1>, 16, wps, sizeof(float2) * Geo<16>::floats2, "scat  Q=16 sync");
     run(body<16, 2, 2>, 16, wps, sizeof(float2) * Geo<16>::floats2, "scat  Q=16 sync/2");
