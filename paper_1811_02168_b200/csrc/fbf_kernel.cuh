@@ -176,11 +176,15 @@ struct Params {
         mbar_wait(bar, par);                    \
         _pw[k] += clock64() - _t0;              \
     } while (0)
+// BAR.SYNC is deferred-blocking: an independent clock read right after it issues before
+// the barrier completes (tools/microbench/bar_arrive.cu: 3 cycles reported for a 5000-cycle
+// wait). The end time is therefore read behind a shared-memory load, which is ordered
+// after the barrier.
 #define PSYNC(k, id, n)                         \
     do {                                        \
         const long long _t0 = clock64();        \
         named_sync(id, n);                      \
-        _pw[k] += clock64() - _t0;              \
+        _pw[k] += clock_after_barrier() - _t0;  \
     } while (0)
 #else
 #define PWAIT(k, bar, par) mbar_wait(bar, par)
@@ -388,6 +392,19 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ int lane_id_() { return (int)(threadIdx.x & 31); }
+// dev (FBF_PHASES): clock read that cannot issue before a shared-memory load placed after
+// a barrier has returned, i.e. before the barrier completed
+__device__ __forceinline__ long long clock_after_barrier() {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const unsigned v = *reinterpret_cast<volatile unsigned*>(smem_raw);
+    long long t;
+    asm volatile(
+        "{\n.reg .u32 z;\n.reg .u64 zz;\nand.b32 z, %1, 0;\ncvt.u64.u32 zz, z;\nmov.u64 %0, %%clock64;\nadd.u64 %0, %0, zz;\n}\n"
+        : "=l"(t)
+        : "r"(v)
+        : "memory");
+    return t;
+}
 // barrier ids (0 is __syncthreads): gen full/empty, column full/empty, f stage empty
 constexpr int kBarGenFull = 1, kBarGenEmpty = 3, kBarColFull = 5, kBarColEmpty = 7, kBarFsEmpty = 9;
 // ROW -> COL ring handoff of the half-mode rings (two blocks): one CTA-wide named

@@ -47,8 +47,15 @@ for w in range(32):
     elif w == nf + 8: names.append("LOAD")
     else: names.append("-")
 nw = nf + 9
+# fixed layouts: pair mode with 7 pairs (register split) and the c4 kernel (kHalfWgMode, 5 pairs)
+fixed = None
+if mode == 0 and np_ == 7:
+    fixed = [f"GEN{3 - w}" for w in range(4)] + [f"COMB{7 - w}" for w in range(4, 8)] + ["LOAD"] + [f"PAIR{15 - w}" for w in range(9, 16)]
+elif mode == 2 and np_ == 5:
+    fixed = list("GGGGMMMMLCCCCCCCRCCCRRRR")
+    fixed = [{"G": "GEN", "M": "COMB", "L": "LOAD", "C": "COLh", "R": "ROW"}[c] for c in fixed]
 for w in range(32):
     tot, wa, wb, n = buf[4 * w:4 * w + 4]
     if n == 0: continue
-    nm = names[nw - 1 - w] if mode != 2 else "slot"
+    nm = fixed[w] if fixed and w < len(fixed) else names[nw - 1 - w] if mode != 2 and 0 <= nw - 1 - w < len(names) else "slot"
     print(f"warp {w:2d} smsp {w % 4} {nm:6s} cycles/CTA {tot / n:10.0f}  waitA {wa / tot * 100:5.1f}%  waitB {wb / tot * 100:5.1f}%  busy {100 - (wa + wb) / tot * 100:5.1f}%")
