@@ -723,6 +723,11 @@ int filter_on_device(int dev, const HostIO& io, const Window& wd, int width, int
     const long long io_bytes = (long long)in_px * (long long)io.in_elem() + (long long)out_px * io.out_elem();
     int pieces = bands ? (int)std::min<long long>(8, std::max<long long>(1, io_bytes / (4 << 20)))
                        : std::min(wd.n_frames, 16);
+    // very large images: the first piece's H2D and the last piece's kernel + D2H are not
+    // overlapped, so keep pieces near 64 MiB of traffic, up to 32 (c4, 1 GiB in + 1 GiB out:
+    // 8 / 16 / 32 / 64 pieces 28.7 / 26.5 / 25.4 / 26.7 ms per call; c2, 64 MiB each way,
+    // stays at 8: 3.29 ms vs 3.52 / 4.25 at 16 / 32)
+    if (bands && io_bytes > (512LL << 20)) pieces = (int)std::min<long long>(32, io_bytes / (64LL << 20));
     if (bands) pieces = std::max(1, std::min(pieces, wd.out_rows / std::max(64, 4 * r)));
     static const int forced_pieces = env_int("FBF_PIECES");  // tuning override
     if (forced_pieces > 0) pieces = std::max(1, std::min(forced_pieces, bands ? wd.out_rows : wd.n_frames));
