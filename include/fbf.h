@@ -207,6 +207,16 @@ int fbf_fast_bilateral_band_f32_device(const float* d_src, int src_row0, int src
                                        double theta, int K, int T, int R, const double* coeffs,
                                        int border, float* d_dst,
                                        unsigned long long* d_fallbacks, int device, void* stream);
+/* Host-buffer band for one rank (one process per GPU): src holds global rows
+ * [src_row0, src_row0 + src_rows) of a width x height image -- the rank's band plus
+ * the halo fbf_band_source_rows() reports -- and out receives output rows
+ * [out_row0, out_row0 + out_rows). Runs on the default device (fbf_set_device) with
+ * the single-image call's H2D / kernel / D2H pipeline and in-kernel intensity
+ * validation; bit-identical to the same rows of fbf_fast_bilateral_f32 on the whole
+ * image (the band split of fbf_fast_bilateral_bands_f32, one band per process). */
+int fbf_fast_bilateral_band_f32(const float* src, int src_row0, int src_rows, int width, int height,
+                                int out_row0, int out_rows, double theta, int K, int T, int R,
+                                const double* coeffs, int border, float* out, long long* fallbacks);
 /* Device-resident batch: n_frames frames at d_img + f*width*height, one
  * launch on `stream` (CTAs share the (frame, strip, row) units evenly, so the
  * per-segment warm-up rows amortise over the batch). No validation. */

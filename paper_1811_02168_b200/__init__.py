@@ -10,7 +10,7 @@ from .fbf import (BorderPolicy, ComparisonResult, ImageDelta, brute_bilateral, b
                   InvalidArgument, OptimizationReport, OptimizeOptions, PerOrderError, PeriodScanResult,
                   RangeKernelKind, RangeKernelSamples, RangeKernelSpec, SpatialKernel, ToleranceUnreachable,
                   band_source_rows, build_spatial_kernel, fast_bilateral, fast_bilateral_band_device,
-                  fast_bilateral_bands, fast_bilateral_batch, fast_bilateral_batch_device, fast_bilateral_u8, pinned_empty, fast_bilateral_device, fbf_filter, field_image,
+                  fast_bilateral_band, fast_bilateral_bands, fast_bilateral_batch, fast_bilateral_batch_device, fast_bilateral_u8, pinned_empty, fast_bilateral_device, fbf_filter, field_image,
                   fit_error, fit_fixed_period, frequency_of, min_error_over_period, optimize_parameters,
                   random_image, sample_range_kernel, scan_gpu_max_order, scan_period_errors, scan_period_errors_gpu,
                   scene_image, select_parameters,

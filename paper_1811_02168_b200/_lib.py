@@ -58,6 +58,7 @@ SIGNATURES = {
     "fbf_fast_bilateral_batch_f32_device": (_i, [_vp, _i, _i, _i, _d, _i, _i, _i, _dp, _i, _vp, _vp, _i, _vp]),
     "fbf_fast_bilateral_batch_f32": (_i, [_fp, _i, _i, _i, _d, _i, _i, _i, _dp, _i, _fp, _llp, _i]),
     "fbf_fast_bilateral_bands_f32": (_i, [_fp, _i, _i, _d, _i, _i, _i, _dp, _i, _fp, _llp, _i]),
+    "fbf_fast_bilateral_band_f32": (_i, [_fp, _i, _i, _i, _i, _i, _i, _d, _i, _i, _i, _dp, _i, _fp, _llp]),
     "fbf_fast_bilateral_band_f32_device": (_i, [_vp, _i, _i, _i, _i, _i, _i, _d, _i, _i, _i, _dp, _i,
                                                 _vp, _vp, _i, _vp]),
     "fbf_band_source_rows": (_i, [_i, _i, _i, _d, _i, _ip, _ip]),

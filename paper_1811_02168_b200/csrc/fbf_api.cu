@@ -1153,6 +1153,31 @@ int fbf_fast_bilateral_bands_f32(const float* img, int width, int height, double
     return FBF_OK;
 }
 
+int fbf_fast_bilateral_band_f32(const float* src, int src_row0, int src_rows, int width, int height, int out_row0,
+                                int out_rows, double theta, int K, int T, int R, const double* coeffs, int border,
+                                float* out, long long* fallbacks) {
+    int r = 0;
+    int rc = check_args(width, height, theta, K, T, R, coeffs, border, &r);
+    if (rc != FBF_OK) return rc;
+    if (!src || !out) return fail(FBF_EINVAL, "fast_bilateral_band: null buffer");
+    if (out_row0 < 0 || out_rows <= 0 || out_row0 + out_rows > height)
+        return fail(FBF_EINVAL, "fast_bilateral_band: output rows outside the image");
+    int s0 = 0, sn = 0;
+    source_window(height, out_row0, out_rows, r, border, &s0, &sn);
+    if (src_row0 < 0 || src_rows <= 0 || src_row0 + src_rows > height || src_row0 > s0 || src_row0 + src_rows < s0 + sn)
+        return fail(FBF_EINVAL, "fast_bilateral_band: source rows do not cover the band's halo window");
+    Approx a;
+    rc = make_approx(K, T, R, coeffs, a);
+    if (rc != FBF_OK) return rc;
+    long long fb = 0;
+    Window wd{1, src_row0, src_rows, out_row0, out_rows};
+    rc = filter_on_device(g_default_device.load(), HostIO{src, out}, wd, width, height, theta, a, border, &fb, nullptr);
+    if (rc != FBF_OK) return rc;
+    if (fallbacks) *fallbacks += fb;
+    clear_error();
+    return FBF_OK;
+}
+
 int fbf_fast_bilateral_u8(const unsigned char* img, int width, int height, double theta, int K, int T, int R,
                           const double* coeffs, int border, unsigned char* out_u8, float* out_f32,
                           long long* fallbacks) {

@@ -502,6 +502,31 @@ def fast_bilateral_bands(img, kernel: SpatialKernel, approx: FourierApproximatio
     return out
 
 
+def fast_bilateral_band(src, src_row0: int, height: int, out_row0: int, out_rows: int, kernel: SpatialKernel,
+                        approx: FourierApproximation, border=BorderPolicy.symmetric,
+                        diag: FilterDiagnostics | None = None, out: np.ndarray | None = None) -> np.ndarray:
+    """One rank's row band from host buffers (one process per GPU): `src` holds global rows
+    [src_row0, src_row0 + src.shape[0]) of a (height, W) image -- the band plus the halo of
+    band_source_rows() -- and the result is output rows [out_row0, out_row0 + out_rows),
+    bit-identical to the same rows of fast_bilateral on the whole image. Runs on the default
+    device (set_device) with the single-image call's H2D / kernel / D2H pipeline."""
+    a = _as_image(src)
+    c = _approx_args(approx)
+    W = a.shape[1]
+    if out is None:
+        out = np.empty((out_rows, W), dtype=np.float32)
+    elif out.dtype != np.float32 or not out.flags.c_contiguous or out.shape != (out_rows, W):
+        raise InvalidArgument("out must be a C-contiguous float32 array of shape (out_rows, width)")
+    fb = ctypes.c_longlong(0)
+    _check(_lib.load().fbf_fast_bilateral_band_f32(_fptr(a), src_row0, a.shape[0], W, height, out_row0, out_rows,
+                                                   kernel.theta, approx.terms, approx.half_period,
+                                                   approx.dynamic_range, _dptr(c), _border(border), _fptr(out),
+                                                   ctypes.byref(fb)))
+    if diag is not None:
+        diag.fallback_pixels += fb.value
+    return out
+
+
 def band_source_rows(height: int, out_row0: int, out_rows: int, theta: float,
                      border=BorderPolicy.symmetric) -> tuple[int, int]:
     """Global source-row window [row0, row0 + rows) a band needs (halo included)."""

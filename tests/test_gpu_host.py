@@ -120,6 +120,37 @@ def test_bands_pipeline_equals_single_call(gpu, border):
     assert np.array_equal(fb.fast_bilateral_bands(img, k, a, border, n_gpus=0), ref)
 
 
+@pytest.mark.parametrize("border", ["symmetric", "replicate", "zero"])
+def test_host_band_entry_equals_full_image_rows(gpu, border):
+    # fbf_fast_bilateral_band_f32: one rank's band + halo window from host buffers (the
+    # one-process-per-GPU form of the band split), every band bit-identical to the same
+    # rows of the whole-image call; argument errors are InvalidArgument
+    fb = gpu
+    from paper_1811_02168_b200 import shard
+    a = fb.select_parameters(80.0, eps=0.05)
+    k = fb.build_spatial_kernel(10.0)
+    H, W = 700, 333
+    img = fb.field_image(W, H, 64, 5.0, 9)
+    ref = fb.fast_bilateral(img, k, a, border)
+    for world in (2, 3):
+        for rank in range(world):
+            b = shard.band_for_rank(H, rank, world, k.theta, border)
+            win = np.ascontiguousarray(img[b.src_row0:b.src_row0 + b.src_rows])
+            diag = fb.FilterDiagnostics()
+            got = fb.fast_bilateral_band(win, b.src_row0, H, b.out_row0, b.out_rows, k, a, border, diag)
+            assert got.shape == (b.out_rows, W)
+            assert np.array_equal(got, ref[b.out_row0:b.out_row0 + b.out_rows]), (world, rank)
+    # a window that misses the halo, rows outside the image
+    with pytest.raises(fb.InvalidArgument):
+        fb.fast_bilateral_band(img[100:200], 100, H, 100, 100, k, a, border)
+    with pytest.raises(fb.InvalidArgument):
+        fb.fast_bilateral_band(img, 0, H, H - 10, 20, k, a, border)
+    bad = img[:200].copy()
+    bad[50, 7] = 300.0
+    with pytest.raises(fb.InvalidArgument):  # FBF_ERANGE: validate_intensities (filter.cpp:19-23)
+        fb.fast_bilateral_band(bad, 0, H, 0, 100, k, a, border)
+
+
 def test_stage_timings_accumulate(gpu):
     fb = gpu
     a = fb.select_parameters(50.0, K=4)
