@@ -575,7 +575,7 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
         return e && std::strcmp(e, "contig") == 0;
     }();
     p.col_rounds = contig ? 0 : (int)(((long long)job.n_frames * p.n_strips) / grid);
-    // Programmatic dependent launch for short launches (< 1024 output rows per CTA: the
+    // Programmatic dependent launch for short launches (< 512 output rows per CTA: the
     // next grid's launch and prologue overlap this one's drain): c0 24.8 -> 24.0 us,
     // one c3 frame 0.499 -> 0.513. Long launches lose with it (c4 0.701 -> 0.693, c2
     // 0.599 -> 0.591: the dependent grid's CTAs land on SMs in drain order, not launch
@@ -584,16 +584,24 @@ int run_job(DeviceCtx& ctx, const Job& job, double theta, const Approx& a, int b
         const char* v = std::getenv("FBF_PDL");
         return v ? std::atoi(v) : -1;
     }();
-    p.pdl = pdl_env >= 0 ? pdl_env : (p.total_units < 1024LL * grid ? 1 : 0);
+    // (r02e: threshold 1024 -> 512 rows per CTA. Back-to-back c1 launches, 885 rows per CTA,
+    // lose with it: 0.572 without, 0.548-0.557 with; a 2048 x 2048 image at r = 9, K = 4
+    // 0.427 vs 0.364. c0 (55 rows) 24.3 vs 25.7 us and one c3 frame (438 rows) 0.519 vs
+    // 0.508 keep it.)
+    p.pdl = pdl_env >= 0 ? pdl_env : (p.total_units < 512LL * grid ? 1 : 0);
     p.inv_period = a.turns();
 
     // Duo launch for two-chunk plans (c2: K = 9, 9 + 8 pairs): clusters of 2 CTAs, each
     // work share filtered by both ranks at once, rank 1's (num, den) partials handed to
     // rank 0 per step through distributed shared memory -- one launch, no HBM scratch,
-    // the same bits as the two scratch launches. FBF_DUO=0 (dev) keeps the scratch path.
-    static const bool duo_off = std::getenv("FBF_DUO") && std::atoi(std::getenv("FBF_DUO")) == 0;
+    // the same bits as the two scratch launches. FBF_DUO=0 (dev) keeps the scratch path, 1 forces the duo.
+    static const int duo_env = std::getenv("FBF_DUO") ? std::atoi(std::getenv("FBF_DUO")) : -1;  // dev: 0 off, 1 on at any radius
+    const bool duo_off = duo_env == 0;
     auto nkr_of = [](const Chunk& c) { return c.n_k - (c.k_lo == 0 ? 1 : 0); };
-    if (!duo_off && plan.chunks.size() == 2 && plan.mode != fbf_dev::kHalfMode && ctx.num_sms >= 2 &&
+    // Small radii keep the two scratch launches (2048 x 2048, K = 9: r = 6 / 9 / 12 0.283 / 0.392 /
+    // 0.521 with the scratch vs 0.268 / 0.377 / 0.480 as a duo; r = 15 0.550 vs 0.554): a duo step
+    // ends with the cross-CTA handoff, which short steps do not amortise.
+    if (!duo_off && plan.chunks.size() == 2 && plan.mode != fbf_dev::kHalfMode && ctx.num_sms >= 2 && (r >= 14 || duo_env == 1) &&
         nkr_of(plan.chunks[0]) == nkr_of(plan.chunks[1]) &&
         std::max(plan.chunks[0].n_pairs, plan.chunks[1].n_pairs) <= plan.ent->duo_max_pairs[plan.ngb][plan.ncb]) {
         const int clusters = (int)std::max(1LL, std::min<long long>((long long)ctx.num_sms / 2, (want + 1) / 2));

@@ -644,7 +644,11 @@ __global__ void __launch_bounds__(block_threads(1 + 2 * NKR, M), 1)
     // read then: RBP - RB + 1 = 2), every step from g = 2 on so the phases pair up.
     // The split-mode scatter ring (c3) keeps the per-pair mbarriers: its 9-pair
     // launches measured 0.493 -> 0.489 with the CTA-wide barrier (the pairs lockstep).
+#ifdef FBF_DEV_RING_MBAR_MAXR  // dev: half-mode rings through per-pair mbarriers up to this radius
+    constexpr bool RING_NB = (is_half(M) && R > FBF_DEV_RING_MBAR_MAXR) || (M == kSplitMode && !G::SCATTER);
+#else
     constexpr bool RING_NB = is_half(M) || (M == kSplitMode && !G::SCATTER);
+#endif
     static_assert(!RING_NB || RBP - RB + 1 == 2 || RBP == 2, "ROW may run two steps ahead of COL");
     static_assert(kBarFsEmpty + NFS <= kBarRingFull, "named barrier ids overlap");
     const int ring_threads = (is_half(M) ? 3 : 2) * nrole;
