@@ -390,7 +390,7 @@ def main():
         single_value = None
     else:
         if world == 1:
-            # the whole image through the public single-image call (8 pipelined row bands)
+            # the whole image through the public single-image call (row bands pipelined inside: up to 8, 32 for very large images)
             a_in = fb.pinned_empty(full.shape)
             a_in[:] = full
             a_out = fb.pinned_empty(full.shape)
